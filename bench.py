@@ -1,0 +1,474 @@
+#!/usr/bin/env python
+"""Headline benchmark: Gauss-Newton Hessian-vector products per second at
+128^3 (K=32 band), Nt=10, fp64 — BASELINE.json config 3 ("EPDiff" variant,
+mapped to the reference's DeformationObjective).
+
+One *step* = one ``Evaluation.hessian_vector(w, gauss_newton=True)`` at a
+fixed evaluation point (the unit of work inside every PCG iteration).  Inputs
+follow the SURVEY §8(d) micro-benchmark recipe (``band_image`` pair, smooth
+``v`` / ``w``, seed 0), generated on the device.  The HVP working set
+(multi-GB stage caches) is far larger than the 126 MB L2, so no explicit L2
+flush is needed between steps.
+
+Arms:
+  default           the B200 path; prints one JSON line with value, e2e
+                    (host-pinned inputs/outputs through the public API),
+                    roofline of the dominant kernel, cpu_baseline, clocks.
+  --impl reference  the reference algorithm on the host CPU (the oracle port
+                    in ``oracle/``, all host threads), bounded samples.
+
+Multi-GPU (torchrun): one independent registration pair per rank (the batch
+configuration shards pairs, no data-path collective); value = sum over ranks,
+timed as the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Hessian-vector products/sec and s/registration at 128^3 (32^3 band, Nt=10); % HBM roofline"
+UNIT = "HVP/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--objective", choices=["deformation", "state"], default="deformation")
+    ap.add_argument("--dtype", choices=["float64", "float32"], default="float64")
+    ap.add_argument("--size", type=int, default=128)
+    ap.add_argument("--band", type=int, default=32)
+    ap.add_argument("--nt", type=int, default=10)
+    ap.add_argument("--registration", type=int, default=1, help="also time one full GN registration")
+    ap.add_argument("--cpu-baseline", type=int, default=1)
+    ap.add_argument("--profile-only", action="store_true", help="one instrumented HVP, no timing")
+    return ap.parse_args()
+
+
+def workload(args):
+    return {"workload": f"{args.objective}_gn_hvp_{args.size}^3_K{args.band}_Nt{args.nt}",
+            "objective": args.objective, "grid": [args.size] * 3, "bandwidth": [args.band] * 3,
+            "n_time_steps": args.nt, "sigma2": 0.1, "alpha": 0.02, "order": 2,
+            "l2": "working set (GB-scale stage caches) >> 126 MB L2; no flush needed"}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[2:]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# synthetic inputs (SURVEY.md §8(d) recipe, generated through the product API)
+# ---------------------------------------------------------------------------
+
+def _freq(m):
+    k = (m - 1) // 2
+    return np.concatenate([np.arange(0, k + 1), np.arange(-k, 0)])
+
+
+def smooth_vector_block(dom, rng, scale, decay):
+    """tests/helpers.py:22-37 recipe on the device: symmetrize, power-law decay,
+    normalise the max-norm of the realization to ``scale``."""
+    from paper_1807_05117_b200 import spectral
+
+    sh = (dom.ndim,) + dom.block_shape
+    c = rng.standard_normal(sh) + 1j * rng.standard_normal(sh)
+    c = spectral.symmetrize(dom, c)
+    k2 = np.zeros(dom.block_shape)
+    for ax, m in enumerate(dom.block_shape):
+        shp = [1] * dom.ndim
+        shp[ax] = m
+        k2 = k2 + (_freq(m).astype(float) ** 2).reshape(shp)
+    import torch
+
+    c = c / torch.from_numpy((1.0 + k2) ** decay).to(c.device)
+    return c * (scale / spectral.max_abs(dom, c))
+
+
+def band_image(dom, rng, decay=3.0):
+    from paper_1807_05117_b200 import spectral
+
+    c = smooth_vector_block(dom, rng, 1.0, decay)[0]
+    img = spectral.include(dom, c)
+    img = img - img.min()
+    return img / img.max()
+
+
+def blob_pair(dom, seed=1):
+    """Seeded 3-D registration pair: periodic bumps, target = source warped
+    (cubic) by a smooth ~3-voxel displacement (the reference's pairs are 2-D)."""
+    import torch
+
+    from paper_1807_05117_b200 import Domain, gridops, spectral
+
+    n = dom.shape[0]
+    rng = np.random.default_rng(seed)
+    axes = [np.arange(s) / s for s in dom.shape]
+    mesh = np.meshgrid(*axes, indexing="ij")
+    src = np.zeros(dom.shape)
+    for _ in range(6):
+        c = 0.3 + 0.4 * rng.random(3)
+        sharp = 8.0 + 16.0 * rng.random()
+        b = np.ones(dom.shape)
+        for x, cc in zip(mesh, c):
+            b = b * np.exp(sharp * (np.cos(2 * np.pi * (x - cc)) - 1.0))
+        src += (0.5 + 0.5 * rng.random()) * b
+    src /= src.max()
+    ddom = Domain(dom.shape, (4,) * dom.ndim, dtype=dom.dtype, device=dom.device)
+    disp = spectral.include(ddom, smooth_vector_block(ddom, rng, 3.0 / n, 2.0))
+    tgt = gridops.warp(ddom, torch.from_numpy(src), disp, "cubic")
+    return src, tgt.double().cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """Per-category DRAM bytes per launch from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def run_b200(args, rank, world, local):
+    import torch
+
+    import paper_1807_05117_b200 as B
+    from paper_1807_05117_b200 import _lib
+
+    torch.cuda.set_device(local)
+    dom = B.Domain((args.size,) * 3, (args.band,) * 3, alpha=0.02, order=2, dtype=args.dtype,
+                   device=local)
+    rng = np.random.default_rng(0)
+    I0 = band_image(dom, rng)
+    I1 = band_image(dom, rng)
+    v = B.TimeFlow(dom, smooth_vector_block(dom, rng, 0.5 / args.size, 2.0)[None], args.nt, True)
+    w = B.TimeFlow(dom, smooth_vector_block(dom, rng, 0.5 / args.size, 2.0)[None], args.nt, True)
+    cls = B.DeformationObjective if args.objective == "deformation" else B.StateObjective
+    cfg = B.ProblemConfig(sigma2=0.1, n_time_steps=args.nt)
+    obj = cls(dom, I0, I1, cfg)
+    ev = obj.gradient(v)
+    torch.cuda.synchronize()
+
+    # instrumented pass: per-kernel-category time and algorithmic bytes
+    _lib.profile_enable(True)
+    ev.hessian_vector(w, gauss_newton=True)
+    torch.cuda.synchronize()
+    prof = _lib.profile_report()
+    _lib.profile_enable(False)
+    if args.profile_only:
+        if rank == 0:
+            print(json.dumps({"profile": prof}))
+        return
+
+    for _ in range(args.warmup):
+        ev.hessian_vector(w, gauss_newton=True)
+    torch.cuda.synchronize()
+    barrier(world)
+    stream = torch.cuda.current_stream()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = _lib.launch_count()
+    with Clocks(local) as clocks:
+        torch.cuda.synchronize()
+        start.record(stream)
+        for _ in range(args.steps):
+            out = ev.hessian_vector(w, gauss_newton=True)
+        end.record(stream)
+        torch.cuda.synchronize()
+    launches = (_lib.launch_count() - l0)
+    barrier(world)
+    t_ms = start.elapsed_time(end)
+    t_ms = max_over_ranks(t_ms, world)
+    per_step_ms = t_ms / args.steps
+    value = world * args.steps / (t_ms / 1e3)
+
+    # end to end through the public API with pinned host buffers
+    host_w = torch.from_numpy(w.values.cpu().numpy()).pin_memory()
+    host_out = torch.empty_like(host_w).pin_memory()
+    dev_w = torch.empty_like(w.values)
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        dev_w.copy_(host_w, non_blocking=True)
+        hv = ev.hessian_vector(B.TimeFlow(dom, dev_w, args.nt, True), gauss_newton=True)
+        host_out.copy_(hv.values, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
+    e2e_value = world * args.steps / (e2e_ms / 1e3)
+    assert torch.equal(host_out, out.values.cpu()), "e2e result differs from the device-resident run"
+
+    # s/registration: one full Gauss-Newton-Krylov registration of a 3-D pair
+    reg = None
+    if args.registration:
+        src, tgt = blob_pair(dom)
+        robj = cls(dom, src, tgt, B.ProblemConfig(sigma2=0.03, n_time_steps=args.nt))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = B.minimize(robj, B.TimeFlow.zero(dom, args.nt), B.SolverConfig())
+        torch.cuda.synchronize()
+        reg_s = max_over_ranks(time.perf_counter() - t0, world)
+        jd = B.gridops.jacobian_determinant(
+            dom, B.spectral.include(dom, res.evaluation.cache.forward[-1], check=False))
+        reg = {"s_per_registration": reg_s, "status": res.status, "outer": len(res.records),
+               "pcg_total": res.total_pcg_iters, "final_mse_rel": res.final_mse_rel,
+               "j_min": float(jd.min()), "j_max": float(jd.max()),
+               "calls": {k: (v if not isinstance(v, list) else
+                             {"n": len(v), "mean_substeps": float(np.mean(v)) if v else 0.0})
+                         for k, v in res.counters.items()},
+               "pair": "6 periodic bumps, target = cubic warp by band-4 displacement (3 vox)"}
+
+    # roofline of the dominant kernel category (live CUDA events)
+    peak, peak_kind = peaks()
+    traffic = ncu_traffic()
+    total_prof_ms = sum(v[1] for v in prof.values())
+    breakdown = {k: {"launches": int(v[0]), "ms": round(v[1], 4),
+                     "share": round(v[1] / total_prof_ms, 4) if total_prof_ms else None,
+                     "gbs": round(v[2] / (v[1] * 1e-3) / 1e9, 1) if v[1] > 0 else None}
+                 for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])}
+    dom_name, dv = max(prof.items(), key=lambda kv: kv[1][1])
+    n_launch, ms, nbytes = dv
+    achieved = nbytes / n_launch / (ms / n_launch * 1e-3) / 1e9
+    tr = traffic.get(dom_name)
+    roofline = {"bound": "hbm", "kernel": dom_name, "achieved": round(achieved, 1), "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                "traffic": tr, "algorithmic_bytes_per_launch": nbytes / n_launch,
+                "avg_launch_us": ms / n_launch * 1e3}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": per_step_ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64" if args.dtype == "float64" else "f32",
+        "data": "synthetic (band_image pair + smooth v, w; SURVEY §8(d) recipe, seed 0)",
+        "config": {**workload(args), "pad": list(dom.pad), "parallelism": f"replicas x{world}"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": host_w.numel() * host_w.element_size(),
+                "d2h_bytes_per_step": host_out.numel() * host_out.element_size()},
+        "gpu_launches": launches,
+        "roofline": roofline,
+        "kernel_breakdown": breakdown,
+        "clocks": clocks.summary(),
+    }
+    if reg:
+        line["registration"] = reg
+    if rank == 0 and world == 1 and args.cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, sample="one")
+    if rank == 0:
+        print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline / reference arm (oracle port on the host cores)
+# ---------------------------------------------------------------------------
+
+def cpu_hvp_sample(args):
+    """Time the pieces of one GN HVP of the reference algorithm on the host
+    (oracle port, scipy.fft on all host threads) and scale to a whole HVP:
+    forward tangent stage x 4*Nt (+ momentum stage x 4*Nt + 11 node
+    contractions for the deformation objective).  Returns (seconds_per_hvp,
+    sample_seconds, description)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import blreg_oracle as O
+
+    O.WORKERS = os.cpu_count() or 1
+    n, k, nt = args.size, args.band, args.nt
+    dom = O.Dom((n,) * 3, (k,) * 3, alpha=0.02, order=2)
+    rng = np.random.default_rng(0)
+    u = O.smooth_vector_block(dom, rng, 0.5 / n, 2.0)
+    du = O.smooth_vector_block(dom, rng, 0.5 / n, 2.0)
+    v = O.smooth_vector_block(dom, rng, 0.5 / n, 2.0)
+    dv = O.smooth_vector_block(dom, rng, 0.5 / n, 2.0)
+    t0 = time.perf_counter()
+    O.rhs_map(dom, u, v)
+    O.rhs_map_tangent(dom, u, du, v, dv)
+    t_fwd = time.perf_counter() - t0
+    stages = 4 * nt
+    total = stages * t_fwd
+    desc = f"1 forward-tangent RK4 stage (rhs_map + rhs_map_tangent) x{stages}"
+    if args.objective == "deformation":
+        t0 = time.perf_counter()
+        O.rhs_momentum_pair(dom, u, du, v, None)
+        t_mom = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        O.conv_matvec(dom, O.jac(dom, u), du, transpose=True)
+        t_con = time.perf_counter() - t0
+        total += stages * t_mom + (nt + 1) * t_con
+        desc += f" + 1 momentum-pair stage x{stages} + 1 node contraction x{nt + 1}"
+        sample = t_fwd + t_mom + t_con
+    else:
+        t0 = time.perf_counter()
+        img = np.random.default_rng(1).random(dom.shape)
+        disp = O.include(dom, u, check=False)
+        O.warp(dom, img, disp)
+        t_w = time.perf_counter() - t0
+        total += (nt + 1) * t_w
+        desc += f" + 1 node warp x{nt + 1}"
+        sample = t_fwd + t_w
+    return total, sample, desc + f" at {n}^3/K={k}, pad {dom.pad_shape[0]} (reference pad)"
+
+
+def cpu_baseline(args, sample="one"):
+    total, sample_s, desc = cpu_hvp_sample(args)
+    return {"value": 1.0 / total, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
+            "sample": desc, "sample_seconds": round(sample_s, 2),
+            "seconds_per_hvp_estimated": round(total, 2)}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        cpu_hvp_sample(args)
+    per = []
+    t0 = time.perf_counter()
+    desc = ""
+    for _ in range(args.steps):
+        total, _, desc = cpu_hvp_sample(args)
+        per.append(total)
+    wall = time.perf_counter() - t0
+    value = 1.0 / float(np.mean(per))
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(per)), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (SURVEY §8(d) recipe, seed 0)", "impl": "reference",
+            "config": {**workload(args), "parallelism": "host CPU"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count() or 1,
+                             "kind": "port", "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": wall}
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        run_reference(args, rank, world)
+        return
+    rank, world, local = dist_setup()
+    try:
+        run_b200(args, rank, world, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -51,6 +51,12 @@ const char* blr_last_error(void);
 /* number of kernels this library launched since load (all contexts) */
 int64_t blr_launch_count(void);
 int blr_version(void);
+/* CUDA-event profiler over kernel categories (scatter, gather, cuFFT, products,
+ * RK4 updates, warps, ...).  Off by default; when on, every instrumented launch
+ * records events on its stream.  report: JSON {"name": [launches, total_ms,
+ * algorithmic_bytes], ...} of everything recorded since the last report. */
+int blr_profile_enable(int on);
+int blr_profile_report(char* buf, int64_t len);
 
 /* ---- spectral algebra (spectral.py) -------------------------------------- */
 

@@ -27,6 +27,8 @@ SIGNATURES = {
     "blr_last_error": [],
     "blr_launch_count": [],
     "blr_version": [],
+    "blr_profile_enable": [_i],
+    "blr_profile_report": [C.c_char_p, _i64],
     "blr_include": [_vp, _i, _vp, _i, _ip, _vp],
     "blr_project": [_vp, _i, _vp, _i, _vp],
     "blr_helmholtz": [_vp, _vp, _i, _i, _vp],
@@ -106,6 +108,19 @@ def check(rc: int, name: str):
 
 def call(name: str, *args):
     check(getattr(load(), name)(*args), name)
+
+
+def profile_enable(on: bool = True):
+    call("blr_profile_enable", int(bool(on)))
+
+
+def profile_report() -> dict:
+    """Per-category {name: (launches, total_ms, algorithmic_bytes)} since the last report."""
+    import json
+
+    buf = C.create_string_buffer(1 << 16)
+    call("blr_profile_report", buf, len(buf))
+    return {k: tuple(v) for k, v in json.loads(buf.value.decode()).items()}
 
 
 def int_array(values):

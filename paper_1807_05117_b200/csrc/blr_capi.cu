@@ -48,6 +48,19 @@ const char* blr_last_error(void) { return g_err.c_str(); }
 int64_t blr_launch_count(void) { return launch_count(); }
 int blr_version(void) { return 1; }
 
+int blr_profile_enable(int on) {
+  return guarded([&] { profile_enable(on != 0); });
+}
+
+int blr_profile_report(char* buf, int64_t len) {
+  return guarded([&] {
+    need(buf && len > 0, "bad arguments");
+    std::string r = profile_report();
+    if ((int64_t)r.size() + 1 > len) throw Error(1, "buffer too small for profile report");
+    std::memcpy(buf, r.c_str(), r.size() + 1);
+  });
+}
+
 int blr_ctx_create(blr_ctx** out, int ndim, const int* shape, const int* bandwidth, const int* pad,
                    double alpha, int order, const double* symbol_tab, int dtype, int device) {
   return guarded([&] {

@@ -198,6 +198,7 @@ void warp(blr_ctx* c, const T* f, int nimg, const T* disp, int n_disp, int inter
     bspline_prefilter<T>(c, f, nimg, coef);
     src = coef;
   }
+  ProfScope ps(c, "warp", (double)fd.nn * n_disp * (fd.d + 2 * nimg) * sizeof(T));
   k_warp<T><<<grid_blocks(fd.nn * n_disp, 256), 256, 0, c->stream>>>(src, nimg, disp, n_disp, interp,
                                                                       fd, out);
   BLR_LAUNCHED();
@@ -362,6 +363,7 @@ void state_gn_accumulate(blr_ctx* c, const T* dlam, const T* vol, const T* psi, 
     bspline_prefilter<T>(c, dlam, 1, coef);
     src = coef;
   }
+  ProfScope ps(c, "state_gn_accumulate", (double)fd.nn * (n_nodes * (1 + 2 * fd.d) + 1 + fd.d) * sizeof(T));
   k_state_gn<T><<<grid_blocks(fd.nn, 256), 256, 0, c->stream>>>(src, vol, psi, gm, n_nodes, dw, interp,
                                                                  fd, acc);
   BLR_LAUNCHED();
@@ -455,6 +457,7 @@ void state_data(blr_ctx* c, const T* vol, const T* lamw, const T* gm, int n_node
     BLR_CUDA(cudaMallocAsync((void**)&dw, n_nodes * sizeof(double), c->stream));
     BLR_CUDA(cudaMemcpyAsync(dw, weights, n_nodes * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   }
+  ProfScope ps(c, "state_data", (double)fd.nn * (n_nodes * (2 + fd.d) + fd.d) * sizeof(T));
   k_state_data<T><<<grid_blocks(fd.nn, 256), 256, 0, c->stream>>>(vol, lamw, gm, n_nodes, dw, fd, out);
   BLR_LAUNCHED();
   if (dw) BLR_CUDA(cudaFreeAsync(dw, c->stream));

@@ -27,6 +27,19 @@ struct ScatterArgs {
 
 int64_t launch_count();
 
+// Per-kernel-category CUDA-event profiler (off by default).  When enabled,
+// each instrumented launch records start/stop events on the launching stream
+// plus the kernel's algorithmic bytes; blr_profile_report() aggregates them.
+bool profiling();
+struct ProfScope {
+  int slot = -1;
+  cudaStream_t stream = nullptr;
+  ProfScope(blr_ctx* c, const char* name, double bytes);
+  ~ProfScope();
+};
+void profile_enable(bool on);
+std::string profile_report();
+
 template <typename T> void realize(blr_ctx* c, bool pad, const std::vector<ScatterField<T>>& fields, T* out);
 template <typename T> void project(blr_ctx* c, bool pad, T* in, int nf, Cx<T>* out);
 template <typename T> ScatterField<T> fld(const Cx<T>* src, int axis);

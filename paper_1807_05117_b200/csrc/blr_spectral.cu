@@ -11,6 +11,7 @@
 
 #include <cmath>
 #include <cstring>
+#include <cstdio>
 #include <mutex>
 
 namespace blr {
@@ -21,6 +22,82 @@ namespace blr {
 static std::atomic<int64_t> g_launches{0};
 void count_launch(int n) { g_launches += n; }
 int64_t launch_count() { return g_launches.load(); }
+
+// ---------------------------------------------------------------------------
+// profiler
+// ---------------------------------------------------------------------------
+namespace {
+struct ProfRec {
+  std::string name;
+  double bytes;
+  cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+std::vector<cudaEvent_t> g_event_pool;
+
+cudaEvent_t take_event() {
+  if (!g_event_pool.empty()) {
+    cudaEvent_t e = g_event_pool.back();
+    g_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
+bool profiling() { return g_prof_on; }
+void profile_enable(bool on) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_on = on;
+}
+
+ProfScope::ProfScope(blr_ctx* c, const char* name, double bytes) {
+  if (!g_prof_on) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  ProfRec r{name, bytes, take_event(), take_event()};
+  stream = c->stream;
+  cudaEventRecord(r.a, stream);
+  slot = (int)g_prof.size();
+  g_prof.push_back(r);
+}
+
+ProfScope::~ProfScope() {
+  if (slot < 0) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  cudaEventRecord(g_prof[slot].b, stream);
+}
+
+std::string profile_report() {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  struct Agg { int64_t n = 0; double ms = 0, bytes = 0; };
+  std::map<std::string, Agg> agg;
+  for (auto& r : g_prof) {
+    cudaEventSynchronize(r.b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    auto& a = agg[r.name];
+    a.n += 1;
+    a.ms += ms;
+    a.bytes += r.bytes;
+    g_event_pool.push_back(r.a);
+    g_event_pool.push_back(r.b);
+  }
+  g_prof.clear();
+  std::string out = "{";
+  bool first = true;
+  for (auto& kv : agg) {
+    char buf[256];
+    snprintf(buf, sizeof(buf), "%s\"%s\": [%lld, %.6f, %.1f]", first ? "" : ", ", kv.first.c_str(),
+             (long long)kv.second.n, kv.second.ms, kv.second.bytes);
+    out += buf;
+    first = false;
+  }
+  return out + "}";
+}
 
 void check_cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw Error(2, std::string(what) + ": " + cudaGetErrorString(e));
@@ -81,6 +158,9 @@ template <typename T>
 void exec_c2r(blr_ctx* c, bool pad, int batch, Cx<T>* in, T* out) {
   cufftHandle h = get_plan(c, pad, batch, false);
   BLR_FFT(cufftSetStream(h, c->stream));
+  GridDesc gd = c->g.grid(pad);
+  ProfScope ps(c, pad ? "cufft_c2r_pad" : "cufft_c2r_full",
+               (double)batch * (gd.half_size() * sizeof(Cx<T>) + gd.real_size() * sizeof(T)));
   if constexpr (sizeof(T) == 8)
     BLR_FFT(cufftExecZ2D(h, (cufftDoubleComplex*)in, (cufftDoubleReal*)out));
   else
@@ -92,6 +172,9 @@ template <typename T>
 void exec_r2c(blr_ctx* c, bool pad, int batch, T* in, Cx<T>* out) {
   cufftHandle h = get_plan(c, pad, batch, true);
   BLR_FFT(cufftSetStream(h, c->stream));
+  GridDesc gd = c->g.grid(pad);
+  ProfScope ps(c, pad ? "cufft_r2c_pad" : "cufft_r2c_full",
+               (double)batch * (gd.half_size() * sizeof(Cx<T>) + gd.real_size() * sizeof(T)));
   if constexpr (sizeof(T) == 8)
     BLR_FFT(cufftExecD2Z(h, (cufftDoubleReal*)in, (cufftDoubleComplex*)out));
   else
@@ -227,6 +310,11 @@ void realize(blr_ctx* c, bool pad, const std::vector<ScatterField<T>>& fields, T
     a.nf = nf;
     for (int i = 0; i < nf; ++i) a.f[i] = fields[off + i];
     Cx<T>* H = (Cx<T>*)scratch(c, c->half_buf, c->half_bytes, (size_t)nf * hs * sizeof(Cx<T>));
+    int nterms = 0;
+    for (int i = 0; i < nf; ++i) nterms += a.f[i].nterms;
+    const double band_half = (double)gd.B[0] * gd.B[1] * (gd.K[2] + 1);
+    ProfScope ps(c, pad ? "scatter_pad" : "scatter_full",
+                 ((double)nf * hs + nterms * band_half) * sizeof(Cx<T>));
     k_scatter<T><<<grid_blocks(hs * nf, 256), 256, 0, c->stream>>>(a, gd, H);
     BLR_LAUNCHED();
     exec_c2r<T>(c, pad, nf, H, out + off * rs);
@@ -245,6 +333,8 @@ void project(blr_ctx* c, bool pad, T* in, int nf, Cx<T>* out) {
     int n = std::min(kMaxScatter, nf - off);
     Cx<T>* H = (Cx<T>*)scratch(c, c->half_buf, c->half_bytes, (size_t)n * hs * sizeof(Cx<T>));
     exec_r2c<T>(c, pad, n, in + (int64_t)off * rs, H);
+    ProfScope ps(c, pad ? "gather_pad" : "gather_full",
+                 (double)n * ((double)gd.B[0] * gd.B[1] * (gd.K[2] + 1) + nb) * sizeof(Cx<T>));
     k_gather<T><<<grid_blocks(nb * n, 256), 256, 0, c->stream>>>(H, gd, n, scale,
                                                                  out + (int64_t)off * nb);
     BLR_LAUNCHED();
@@ -437,6 +527,7 @@ __global__ void k_flux_div(const Cx<T>* F, int nsets, int d, BandDesc bd, Cx<T>*
 template <typename T>
 void band_flux_div(blr_ctx* c, const Cx<T>* F, int nsets, Cx<T>* out) {
   BandDesc bd = band_desc(c->g);
+  ProfScope ps(c, "band_epilogue", (double)bd.nb * nsets * (c->g.d * c->g.d + c->g.d) * sizeof(Cx<T>));
   k_flux_div<T><<<grid_blocks(bd.nb * c->g.d * nsets, 256), 256, 0, c->stream>>>(F, nsets, c->g.d,
                                                                                  bd, out);
   BLR_LAUNCHED();
@@ -488,6 +579,7 @@ __global__ void k_neg_add(const Cx<T>* a, const Cx<T>* b, Cx<T>* out, int64_t n)
 
 template <typename T>
 void band_neg_add(blr_ctx* c, const Cx<T>* a, const Cx<T>* b, Cx<T>* out, int64_t n) {
+  ProfScope ps(c, "band_epilogue", 3.0 * n * sizeof(Cx<T>));
   k_neg_add<T><<<grid_blocks(n, 256), 256, 0, c->stream>>>(a, b, out, n);
   BLR_LAUNCHED();
 }
@@ -531,6 +623,7 @@ __global__ void k_rk4(int s, const Cx<T>* k, Cx<T>* cur, Cx<T>* acc, Cx<T>* stag
 template <typename T>
 void band_rk4(blr_ctx* c, int s, const Cx<T>* k, Cx<T>* cur, Cx<T>* acc, Cx<T>* stage, double cs,
               double h6, int64_t n) {
+  ProfScope ps(c, "rk4_update", (double)n * sizeof(Cx<T>) * (s == 1 ? 3 : (s < 4 ? 5 : 4)));
   k_rk4<T><<<grid_blocks(n, 256), 256, 0, c->stream>>>(s, k, cur, acc, stage, (T)cs, (T)h6, n);
   BLR_LAUNCHED();
 }

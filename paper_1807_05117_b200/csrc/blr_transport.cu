@@ -107,6 +107,15 @@ template <typename T, int OP>
 static void prod(blr_ctx* c, ProdArgs<T> p) {
   p.np = c->g.np();
   p.d = c->g.d;
+  const int d = p.d;
+  double fields = 0;
+  if (OP == kMatVec) fields = (p.M2 ? 2 : 1) * (d * d + d) + d;
+  if (OP == kMatVecT) fields = d * d + 2 * d;
+  if (OP == kMatVecAcc) fields = d * d + 3 * d;
+  if (OP == kVolume) fields = 2 * d + 3;
+  if (OP == kVolumeT) fields = 4 * d + 5;
+  if (OP == kOuter) fields = (p.a2 ? 4 * d : 2 * d) + d * d;
+  ProfScope ps(c, "pad_product", fields * p.np * sizeof(T));
   k_prod<T, OP><<<grid_blocks(p.np, 256), 256, 0, c->stream>>>(p);
   BLR_LAUNCHED();
 }
