@@ -115,6 +115,7 @@ int blr_ctx_destroy(blr_ctx* c) {
   return guarded([&] {
     if (!c) return;
     cudaStreamSynchronize(c->stream);
+    pad_engine_release(c);
     for (auto& kv : c->plans) cufftDestroy(kv.second);
     for (void* p : {(void*)c->d_sym, c->fft_work, c->real_buf, c->half_buf, c->band_buf, c->full_buf,
                     (void*)c->d_red})

@@ -82,6 +82,20 @@ template <typename T> void contract(blr_ctx* c, const Cx<T>* phi, const Cx<T>* r
 template <typename T> void conv_matvec(blr_ctx* c, const Cx<T>* M, const Cx<T>* x, bool transpose, Cx<T>* out);
 
 
+// fused pad engine (blr_pad.cu); each returns false when unavailable (v1 fallback)
+template <typename T> bool pad_engine_ok(blr_ctx* c);
+void pad_engine_release(blr_ctx* c);
+template <typename T> bool forward_map_v2(blr_ctx* c, FlowRef v, int substeps, Cx<T>* phi, T* du_cache);
+template <typename T> bool inverse_map_and_volume_v2(blr_ctx* c, FlowRef v, int substeps, Cx<T>* psi, Cx<T>* vol);
+template <typename T> bool state_tangents_v2(blr_ctx* c, FlowRef v, FlowRef dv, int substeps, int flags,
+                                             const T* du_cache, Cx<T>* dphi, Cx<T>* dpsi, Cx<T>* dvol);
+template <typename T> bool momentum_v2(blr_ctx* c, FlowRef v, int substeps, const Cx<T>* rho_end, Cx<T>* rho);
+template <typename T> bool momentum_pair_v2(blr_ctx* c, FlowRef v, FlowRef dv, int substeps, const Cx<T>* rho_end,
+                                            const Cx<T>* drho_end, Cx<T>* rho, Cx<T>* drho);
+template <typename T> bool contract_v2(blr_ctx* c, const Cx<T>* phi, const Cx<T>* rho, int n_nodes,
+                                       const double* weights, bool transpose, T* dphi_cache, int cache_mode,
+                                       Cx<T>* out);
+
 // full grid (blr_grid.cu)
 template <typename T> void warp(blr_ctx* c, const T* f, int nimg, const T* disp, int n_disp, int interp, T* out);
 template <typename T> void grid_gradient(blr_ctx* c, const T* f, int nf, int mode, T* out);

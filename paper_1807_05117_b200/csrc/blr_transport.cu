@@ -297,6 +297,7 @@ static void push_grad(const Geom& g, const Cx<T>* s, std::vector<ScatterField<T>
 // ---------------------------------------------------------------------------
 template <typename T>
 void forward_map(blr_ctx* c, FlowRef v, int substeps, Cx<T>* phi, T* du_cache) {
+  if (forward_map_v2<T>(c, v, substeps, phi, du_cache)) return;
   const Geom& g = c->g;
   const int d = g.d;
   const int64_t nb = g.nb(), np = g.np(), L = d * nb;
@@ -325,6 +326,7 @@ void forward_map(blr_ctx* c, FlowRef v, int substeps, Cx<T>* phi, T* du_cache) {
 
 template <typename T>
 void inverse_map_and_volume(blr_ctx* c, FlowRef v, int substeps, Cx<T>* psi, Cx<T>* vol) {
+  if (inverse_map_and_volume_v2<T>(c, v, substeps, psi, vol)) return;
   const Geom& g = c->g;
   const int d = g.d;
   const int64_t nb = g.nb(), np = g.np(), L = (d + 1) * nb;
@@ -363,6 +365,7 @@ void inverse_map_and_volume(blr_ctx* c, FlowRef v, int substeps, Cx<T>* psi, Cx<
 template <typename T>
 void state_tangents(blr_ctx* c, FlowRef v, FlowRef dv, int substeps, int flags, const T* du_cache,
                     Cx<T>* dphi, Cx<T>* dpsi, Cx<T>* dvol) {
+  if (state_tangents_v2<T>(c, v, dv, substeps, flags, du_cache, dphi, dpsi, dvol)) return;
   const Geom& g = c->g;
   const int d = g.d;
   const int64_t nb = g.nb(), np = g.np();
@@ -492,6 +495,7 @@ void state_tangents(blr_ctx* c, FlowRef v, FlowRef dv, int substeps, int flags, 
 
 template <typename T>
 void momentum(blr_ctx* c, FlowRef v, int substeps, const Cx<T>* rho_end, Cx<T>* rho) {
+  if (momentum_v2<T>(c, v, substeps, rho_end, rho)) return;
   const Geom& g = c->g;
   const int d = g.d;
   const int64_t nb = g.nb(), np = g.np(), L = d * nb;
@@ -528,6 +532,7 @@ void momentum_tangent(blr_ctx* c, FlowRef v, FlowRef dv, int substeps, const Cx<
     momentum<T>(c, v, substeps, drho_end, drho);
     return;
   }
+  if (momentum_pair_v2<T>(c, v, dv, substeps, rho_end, drho_end, rho, drho)) return;
   const Geom& g = c->g;
   const int d = g.d;
   const int64_t nb = g.nb(), np = g.np(), L = 2 * d * nb;
@@ -571,6 +576,7 @@ void momentum_tangent(blr_ctx* c, FlowRef v, FlowRef dv, int substeps, const Cx<
 template <typename T>
 void contract(blr_ctx* c, const Cx<T>* phi, const Cx<T>* rho, int n_nodes, const double* weights,
               bool transpose, T* dphi_cache, int cache_mode, Cx<T>* out) {
+  if (contract_v2<T>(c, phi, rho, n_nodes, weights, transpose, dphi_cache, cache_mode, out)) return;
   const Geom& g = c->g;
   const int d = g.d;
   const int64_t nb = g.nb(), np = g.np(), L = d * nb;
