@@ -1,548 +1,39 @@
-// blr_pad.cu — the fused pad-grid engine (v2) for every truncated
-// convolution on the hot path (transport.py:206-303, deformation.py:63-72).
-//
-// A right-hand side is three kernels, no cuFFT, no full-grid zero padding:
-//
-//   k_inv2d   one CTA per (field, kz) plane: gathers the band plane with the
-//             derivative multiplier (i 2 pi k_j) fused, inverse Stockham FFT
-//             along x then along y in shared memory, writes the plane of the
-//             "S layout" [field][kz][x][y] (kz = 0..K only: Hermitian half).
-//   k_lines   one CTA per (x, y-chunk): per z-line, two-for-one C2R of the
-//             spectral inputs, the pointwise product of the RHS (reading the
-//             cached real pad fields: D(u) stages, v, dv), two-for-one R2C of
-//             the outputs back to the S layout (kz = 0..K).
-//   k_fwd2d   one CTA per (output, kz) plane: forward FFT along y then x,
-//             keeps the band, applies post-transform derivative multipliers
-//             (flux divergence), 1/P^3, symmetrizes the kz = 0 plane, the RHS
-//             epilogue (-(v + .), negation) and the RK4 stage update.
-//
-// Band state lives in the "H layout" [comp][kz 0..K][kx][ky] (Hermitian half);
-// node records are converted back to the reference's full blocks.
-#include "blr_fft.cuh"
-#include "blr_internal.cuh"
+// blr_pad.cu — host orchestration of the fused pad-grid engine: engine setup,
+// length dispatch, realization / projection helpers and the RK4 integrators
+// (kernels: blr_pad_kernels.cuh, instantiated per length in blr_pad_L*.cu).
+#include "blr_pad_kernels.cuh"
 
+#include <array>
 #include <cmath>
 #include <cstring>
 
 namespace blr {
 
-// ---------------------------------------------------------------------------
-// geometry
-// ---------------------------------------------------------------------------
-struct PadGeom {
-  int P[3], K[3], B[3];
-  int Kz1;       // K[2] + 1
-  int64_t nh;    // H-layout component size Kz1*B0*B1
-  int64_t ns;    // S-layout field size Kz1*P0*P1
-  int64_t np;    // real pad field size
-  FftSpec fx, fy, fz;
-  int G;         // line group for the 2-D kernels
-  int Yt;        // lines per CTA in k_lines (set per launch)
-};
-
-__device__ __forceinline__ int bin_to_index(int p, int P, int K, int B) {
-  if (p <= K) return p;
-  if (p >= P - K) return p - P + B;
-  return -1;
-}
-
-template <typename T>
-__device__ __forceinline__ void load_tw(Cx<T>* dst, const double2* src, int n) {
-  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = cx<T>((T)src[i].x, (T)src[i].y);
-}
-
-// ---------------------------------------------------------------------------
-// k_inv2d
-// ---------------------------------------------------------------------------
-constexpr int kMaxInv = 32;
-
-template <typename T>
-struct InvField {
-  const Cx<T>* src[3];  // H-layout component bases
-  int axis[3];          // derivative 3-axis or -1
-  int nterms;
-};
-
-template <typename T>
-struct InvArgs {
-  InvField<T> f[kMaxInv];
-  int nf;
-};
-
-template <typename T>
-__global__ void __launch_bounds__(256) k_inv2d(InvArgs<T> a, PadGeom g, const double2* __restrict__ twx_g,
-                                               const double2* __restrict__ twy_g, Cx<T>* __restrict__ out) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int P0 = g.P[0], P1 = g.P[1], B0 = g.B[0], B1 = g.B[1];
-  const int Pm = P0 > P1 ? P0 : P1;
-  Cx<T>* twx = (Cx<T>*)smem_raw;
-  Cx<T>* twy = twx + P0;
-  Cx<T>* Tb = twy + P1;            // [B1][P0]
-  Cx<T>* w0 = Tb + B1 * P0;        // [G][Pm]
-  Cx<T>* w1 = w0 + g.G * Pm;
-  const int f = blockIdx.x / g.Kz1;
-  const int kz = blockIdx.x - f * g.Kz1;
-  const InvField<T> F = a.f[f];
-  load_tw<T>(twx, twx_g, P0);
-  load_tw<T>(twy, twy_g, P1);
-  const int64_t plane = (int64_t)kz * B0 * B1;
-  const T kz_ang = (T)(kTwoPi * (double)kz);
-  __syncthreads();
-  // x-pass over the B1 band columns
-  for (int c0 = 0; c0 < B1; c0 += g.G) {
-    const int ng = min(g.G, B1 - c0);
-    for (int idx = threadIdx.x; idx < ng * P0; idx += blockDim.x) {
-      const int gl = idx / P0, p = idx - gl * P0;
-      const int ix = bin_to_index(p, P0, g.K[0], B0);
-      Cx<T> val = cx<T>(0, 0);
-      if (ix >= 0) {
-        const int iy = c0 + gl;
-        const int64_t off = plane + (int64_t)ix * B1 + iy;
-        for (int t = 0; t < F.nterms; ++t) {
-          Cx<T> z = F.src[t][off];
-          const int ax = F.axis[t];
-          if (ax >= 0) {
-            T k;
-            if (ax == 0) k = (T)(kTwoPi * (double)freq_of(ix, g.K[0], B0));
-            else if (ax == 1) k = (T)(kTwoPi * (double)freq_of(iy, g.K[1], B1));
-            else k = kz_ang;
-            z = cx<T>(-(k * z.y), k * z.x);
-          }
-          val = cadd(val, z);
-        }
-      }
-      w0[gl * P0 + p] = val;
-    }
-    __syncthreads();
-    Cx<T>* r = fft_lines<T, true>(w0, w1, ng, g.fx, twx);
-    for (int idx = threadIdx.x; idx < ng * P0; idx += blockDim.x) Tb[c0 * P0 + idx] = r[idx];
-    __syncthreads();
-  }
-  // y-pass over the P0 rows, straight to global
-  Cx<T>* outp = out + (int64_t)f * g.ns + (int64_t)kz * P0 * P1;
-  for (int x0 = 0; x0 < P0; x0 += g.G) {
-    const int ng = min(g.G, P0 - x0);
-    for (int idx = threadIdx.x; idx < ng * P1; idx += blockDim.x) {
-      const int gl = idx / P1, q = idx - gl * P1;
-      const int iy = bin_to_index(q, P1, g.K[1], B1);
-      w0[gl * P1 + q] = iy >= 0 ? Tb[iy * P0 + x0 + gl] : cx<T>(0, 0);
-    }
-    __syncthreads();
-    Cx<T>* r = fft_lines<T, true>(w0, w1, ng, g.fy, twy);
-    for (int idx = threadIdx.x; idx < ng * P1; idx += blockDim.x) outp[(int64_t)x0 * P1 + idx] = r[idx];
-    __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------------------
-// k_lines
-// ---------------------------------------------------------------------------
-enum LineOp {
-  kOpRealize = 0,   // write realized inputs (wout) only
-  kOpMap = 1,       // out_i = sum_j S[ij] R[j]
-  kOpMapTC = 2,     // out_i = sum_j S[ij] V_j + sum_j Du_ij dV_j   (Du, V, dV real)
-  kOpMapTF = 3,     // out = [Du.V | dDu.V + Du.dV]                 (Du, dDu spectral)
-  kOpInvVol = 4,    // out = [Dw.V | -V.G - J Dv]
-  kOpBwdVol = 5,    // out = [Dw.V | dDw.V + Dw.dV | vol | vol tangent]
-  kOpOuter = 6,     // out_ij = rho_i V_j
-  kOpOuterPair = 7, // out = [rho x V | drho x V + rho x dV]
-  kOpContract = 8,  // out_i = sum_n w_n sum_j M_n(ji or ij) rho_n,j  (M real, cached)
-};
-
-constexpr int kMaxLineS = 28;
-constexpr int kMaxLineR = 16;
-constexpr int kMaxLineO = 18;
-
-template <typename T>
-struct LineArgs {
-  const Cx<T>* sin[kMaxLineS];
-  const T* rin[kMaxLineR];
-  Cx<T>* sout[kMaxLineO];
-  T* wout[kMaxLineS];
-  int ns, nr, no;
-  int d;
-  // contract
-  int n_nodes;
-  int64_t sin_node_stride;  // complex entries between nodes (per input field)
-  int64_t rin_node_stride;  // real entries between nodes
-  double w[32];
-  int transpose;
-};
-
-template <typename T, int OP>
-__device__ __forceinline__ void line_point(const LineArgs<T>& a, const T* Rs, int ldR, int li,
-                                           int64_t gi, T* out, int ldO) {
-  const int d = a.d;
-  auto S = [&](int f) { return Rs[f * ldR + li]; };
-  auto Rg = [&](int f) { return a.rin[f][gi]; };
-  if constexpr (OP == kOpMap) {
-    for (int i = 0; i < d; ++i) {
-      T acc = 0;
-      for (int j = 0; j < d; ++j) acc += S(i * d + j) * Rg(j);
-      out[i * ldO + li] = acc;
-    }
-  } else if constexpr (OP == kOpMapTC) {
-    const int dd = d * d;
-    for (int i = 0; i < d; ++i) {
-      T a1 = 0, a2 = 0;
-      for (int j = 0; j < d; ++j) a1 += S(i * d + j) * Rg(dd + j);
-      for (int j = 0; j < d; ++j) a2 += Rg(i * d + j) * Rg(dd + d + j);
-      out[i * ldO + li] = a1 + a2;
-    }
-  } else if constexpr (OP == kOpMapTF) {
-    const int dd = d * d;
-    for (int i = 0; i < d; ++i) {
-      T b = 0, a1 = 0, a2 = 0;
-      for (int j = 0; j < d; ++j) b += S(i * d + j) * Rg(j);
-      for (int j = 0; j < d; ++j) a1 += S(dd + i * d + j) * Rg(j);
-      for (int j = 0; j < d; ++j) a2 += S(i * d + j) * Rg(d + j);
-      out[i * ldO + li] = b;
-      out[(d + i) * ldO + li] = a1 + a2;
-    }
-  } else if constexpr (OP == kOpInvVol) {
-    const int dd = d * d;
-    for (int i = 0; i < d; ++i) {
-      T b = 0;
-      for (int j = 0; j < d; ++j) b += S(i * d + j) * Rg(j);
-      out[i * ldO + li] = b;
-    }
-    T s = 0;
-    for (int q = 0; q < d; ++q) s += Rg(q) * S(dd + q);
-    out[d * ldO + li] = -s - S(dd + d) * Rg(d);
-  } else if constexpr (OP == kOpBwdVol) {
-    const int dd = d * d;
-    // S: Dw [0,dd) dDw [dd,2dd) G [2dd,2dd+d) dG [2dd+d, 2dd+2d) J, dJ
-    // R: V [0,d) dV [d,2d) Dv 2d dDv 2d+1
-    for (int i = 0; i < d; ++i) {
-      T b = 0, a1 = 0, a2 = 0;
-      for (int j = 0; j < d; ++j) b += S(i * d + j) * Rg(j);
-      for (int j = 0; j < d; ++j) a1 += S(dd + i * d + j) * Rg(j);
-      for (int j = 0; j < d; ++j) a2 += S(i * d + j) * Rg(d + j);
-      out[i * ldO + li] = b;
-      out[(d + i) * ldO + li] = a1 + a2;
-    }
-    const int g0 = 2 * dd, dg0 = 2 * dd + d, jj = 2 * dd + 2 * d;
-    T s = 0, s1 = 0, s2 = 0;
-    for (int q = 0; q < d; ++q) s += Rg(q) * S(g0 + q);
-    out[2 * d * ldO + li] = -s - S(jj) * Rg(2 * d);
-    for (int q = 0; q < d; ++q) s1 += Rg(d + q) * S(g0 + q);
-    for (int q = 0; q < d; ++q) s2 += Rg(q) * S(dg0 + q);
-    out[(2 * d + 1) * ldO + li] = -s1 - s2 - S(jj + 1) * Rg(2 * d) - S(jj) * Rg(2 * d + 1);
-  } else if constexpr (OP == kOpOuter) {
-    for (int i = 0; i < d; ++i) {
-      T r = S(i);
-      for (int j = 0; j < d; ++j) out[(i * d + j) * ldO + li] = r * Rg(j);
-    }
-  } else if constexpr (OP == kOpOuterPair) {
-    const int dd = d * d;
-    for (int i = 0; i < d; ++i) {
-      T r = S(i), dr = S(d + i);
-      for (int j = 0; j < d; ++j) {
-        out[(i * d + j) * ldO + li] = r * Rg(j);
-        out[(dd + i * d + j) * ldO + li] = dr * Rg(j) + r * Rg(d + j);
-      }
-    }
-  }
-}
-
-template <typename T, int OP>
-__global__ void __launch_bounds__(256) k_lines(LineArgs<T> a, PadGeom g, const double2* __restrict__ twz_g) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int P0 = g.P[0], P1 = g.P[1], P2 = g.P[2], K2 = g.K[2];
-  const int Yt = g.Yt;
-  const int nyc = (P1 + Yt - 1) / Yt;
-  const int x = blockIdx.x / nyc;
-  const int y0 = (blockIdx.x - x * nyc) * Yt;
-  const int nl = min(Yt, P1 - y0);
-  const int ns_blk = OP == kOpContract ? a.d : a.ns;
-  const int no_blk = OP == kOpRealize ? 0 : a.no;
-  Cx<T>* twz = (Cx<T>*)smem_raw;
-  Cx<T>* w0 = twz + P2;
-  Cx<T>* w1 = w0 + Yt * P2;
-  T* Rs = (T*)(w1 + Yt * P2);        // [ns_blk][Yt*P2]
-  T* Ro = Rs + ns_blk * Yt * P2;     // [no][Yt*P2]
-  const int ldR = Yt * P2;
-  load_tw<T>(twz, twz_g, P2);
-  const int64_t sline = (int64_t)x * P1 + y0;          // S-layout offset of line 0 at kz = 0
-  const int64_t kzs = (int64_t)P0 * P1;                 // S-layout kz stride
-  const int64_t rline = ((int64_t)x * P1 + y0) * P2;    // R-layout offset of line 0
-  if (OP == kOpContract)
-    for (int i = threadIdx.x; i < no_blk * ldR; i += blockDim.x) Ro[i] = 0;
-  __syncthreads();
-
-  const int nloop = OP == kOpContract ? a.n_nodes : 1;
-  for (int node = 0; node < nloop; ++node) {
-    // ---- realize spectral inputs, two per complex FFT ----
-    for (int f = 0; f < ns_blk; f += 2) {
-      const bool two = f + 1 < ns_blk;
-      const int64_t noff = OP == kOpContract ? node * a.sin_node_stride : 0;
-      const Cx<T>* S1 = a.sin[f] + noff + sline;
-      const Cx<T>* S2 = two ? a.sin[f + 1] + noff + sline : nullptr;
-      for (int idx = threadIdx.x; idx < nl * P2; idx += blockDim.x) {
-        const int l = idx % nl, k = idx / nl;
-        Cx<T> G = cx<T>(0, 0);
-        if (k == 0) {
-          G.x = S1[l].x;
-          G.y = two ? S2[l].x : (T)0;
-        } else if (k <= K2) {
-          Cx<T> F1 = S1[k * kzs + l];
-          Cx<T> F2 = two ? S2[k * kzs + l] : cx<T>(0, 0);
-          G = cx<T>(F1.x - F2.y, F1.y + F2.x);
-        } else if (k >= P2 - K2) {
-          const int kk = P2 - k;
-          Cx<T> F1 = S1[kk * kzs + l];
-          Cx<T> F2 = two ? S2[kk * kzs + l] : cx<T>(0, 0);
-          G = cx<T>(F1.x + F2.y, F2.x - F1.y);
-        }
-        w0[l * P2 + k] = G;
-      }
-      __syncthreads();
-      Cx<T>* r = fft_lines<T, true>(w0, w1, nl, g.fz, twz);
-      T* W1 = (OP != kOpContract) ? a.wout[f] : nullptr;
-      T* W2 = (OP != kOpContract && two) ? a.wout[f + 1] : nullptr;
-      for (int idx = threadIdx.x; idx < nl * P2; idx += blockDim.x) {
-        Cx<T> v = r[idx];
-        Rs[f * ldR + idx] = v.x;
-        if (two) Rs[(f + 1) * ldR + idx] = v.y;
-        if (W1) W1[rline + idx] = v.x;
-        if (W2) W2[rline + idx] = v.y;
-      }
-      __syncthreads();
-    }
-    if (OP == kOpRealize) return;
-    // ---- pointwise products ----
-    for (int idx = threadIdx.x; idx < nl * P2; idx += blockDim.x) {
-      const int64_t gi = rline + idx;
-      if constexpr (OP == kOpContract) {
-        const int d = a.d;
-        const int64_t roff = node * a.rin_node_stride + gi;
-        const T wn = (T)a.w[node];
-        for (int i = 0; i < d; ++i) {
-          T acc = 0;
-          for (int j = 0; j < d; ++j) {
-            const int mi = a.transpose ? (j * d + i) : (i * d + j);
-            acc += a.rin[mi][roff] * Rs[j * ldR + idx];
-          }
-          Ro[i * ldR + idx] += wn * acc;
-        }
-      } else {
-        line_point<T, OP>(a, Rs, ldR, idx, gi, Ro, ldR);
-      }
-    }
-    __syncthreads();
-  }
-  // ---- R2C of the outputs, two per complex FFT ----
-  for (int o = 0; o < no_blk; o += 2) {
-    const bool two = o + 1 < no_blk;
-    for (int idx = threadIdx.x; idx < nl * P2; idx += blockDim.x)
-      w0[idx] = cx<T>(Ro[o * ldR + idx], two ? Ro[(o + 1) * ldR + idx] : (T)0);
-    __syncthreads();
-    Cx<T>* r = fft_lines<T, false>(w0, w1, nl, g.fz, twz);
-    Cx<T>* O1 = a.sout[o] + sline;
-    Cx<T>* O2 = two ? a.sout[o + 1] + sline : nullptr;
-    for (int idx = threadIdx.x; idx < nl * (K2 + 1); idx += blockDim.x) {
-      const int l = idx % nl, k = idx / nl;
-      Cx<T> Z = r[l * P2 + k];
-      Cx<T> Zm = r[l * P2 + (k == 0 ? 0 : P2 - k)];
-      Zm.y = -Zm.y;
-      O1[k * kzs + l] = cx<T>((T)0.5 * (Z.x + Zm.x), (T)0.5 * (Z.y + Zm.y));
-      if (two) O2[k * kzs + l] = cx<T>((T)0.5 * (Z.y - Zm.y), (T)-0.5 * (Z.x - Zm.x));
-    }
-    __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------------------
-// k_fwd2d
-// ---------------------------------------------------------------------------
-constexpr int kMaxFwd = 18;
-enum FwdMode { kEpiPlain = 0, kEpiNeg = 1, kEpiNegAdd = 2 };
-
-template <typename T>
-struct FwdOut {
-  const Cx<T>* sin[3];  // S-layout term fields
-  int axis[3];          // post-transform derivative 3-axis or -1
-  int nterms;
-  int mode;
-  const Cx<T>* vt;      // H-layout component for kEpiNegAdd
-};
-
-template <typename T>
-struct FwdArgs {
-  FwdOut<T> o[kMaxFwd];
-  int no;
-  T scale;
-  Cx<T>* kout;          // H-layout [no][nh] or nullptr
-  int rk_s;             // 0: no RK4 update
-  T cs, h6;
-  Cx<T>* cur;
-  Cx<T>* acc;
-  Cx<T>* stage;
-};
-
-template <typename T>
-__global__ void __launch_bounds__(256) k_fwd2d(FwdArgs<T> a, PadGeom g, const double2* __restrict__ twx_g,
-                                               const double2* __restrict__ twy_g) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int P0 = g.P[0], P1 = g.P[1], B0 = g.B[0], B1 = g.B[1];
-  const int Pm = P0 > P1 ? P0 : P1;
-  Cx<T>* twx = (Cx<T>*)smem_raw;
-  Cx<T>* twy = twx + P0;
-  Cx<T>* Tb = twy + P1;            // [B1][P0]
-  Cx<T>* Rb = Tb + B1 * P0;        // [B0][B1] result
-  Cx<T>* w0 = Rb + B0 * B1;        // [G][Pm]
-  Cx<T>* w1 = w0 + g.G * Pm;
-  const int o = blockIdx.x / g.Kz1;
-  const int kz = blockIdx.x - o * g.Kz1;
-  const FwdOut<T> O = a.o[o];
-  load_tw<T>(twx, twx_g, P0);
-  load_tw<T>(twy, twy_g, P1);
-  for (int i = threadIdx.x; i < B0 * B1; i += blockDim.x) Rb[i] = cx<T>(0, 0);
-  __syncthreads();
-  for (int t = 0; t < O.nterms; ++t) {
-    const Cx<T>* src = O.sin[t] + (int64_t)kz * P0 * P1;
-    // y-pass over rows x, keep band ky
-    for (int x0 = 0; x0 < P0; x0 += g.G) {
-      const int ng = min(g.G, P0 - x0);
-      for (int idx = threadIdx.x; idx < ng * P1; idx += blockDim.x) w0[idx] = src[(int64_t)x0 * P1 + idx];
-      __syncthreads();
-      Cx<T>* r = fft_lines<T, false>(w0, w1, ng, g.fy, twy);
-      for (int idx = threadIdx.x; idx < ng * B1; idx += blockDim.x) {
-        const int gl = idx / B1, iy = idx - gl * B1;
-        const int q = pmod(freq_of(iy, g.K[1], B1), P1);
-        Tb[iy * P0 + x0 + gl] = r[gl * P1 + q];
-      }
-      __syncthreads();
-    }
-    // x-pass over the band columns, keep band kx, accumulate with multiplier
-    const int ax = O.axis[t];
-    for (int c0 = 0; c0 < B1; c0 += g.G) {
-      const int ng = min(g.G, B1 - c0);
-      for (int idx = threadIdx.x; idx < ng * P0; idx += blockDim.x) w0[idx] = Tb[c0 * P0 + idx];
-      __syncthreads();
-      Cx<T>* r = fft_lines<T, false>(w0, w1, ng, g.fx, twx);
-      for (int idx = threadIdx.x; idx < ng * B0; idx += blockDim.x) {
-        const int gl = idx / B0, ix = idx - gl * B0;
-        const int iy = c0 + gl;
-        const int p = pmod(freq_of(ix, g.K[0], B0), P0);
-        Cx<T> z = r[gl * P0 + p];
-        if (ax >= 0) {
-          T k;
-          if (ax == 0) k = (T)(kTwoPi * (double)freq_of(ix, g.K[0], B0));
-          else if (ax == 1) k = (T)(kTwoPi * (double)freq_of(iy, g.K[1], B1));
-          else k = (T)(kTwoPi * (double)kz);
-          z = cx<T>(-(k * z.y), k * z.x);
-        }
-        Rb[ix * B1 + iy] = cadd(Rb[ix * B1 + iy], z);
-      }
-      __syncthreads();
-    }
-  }
-  // scale + symmetrize the kz = 0 plane (pairs handled by one thread)
-  const T sc = a.scale;
-  for (int e = threadIdx.x; e < B0 * B1; e += blockDim.x) {
-    const int ix = e / B1, iy = e - ix * B1;
-    if (kz == 0) {
-      const int mx = ix == 0 ? 0 : B0 - ix, my = iy == 0 ? 0 : B1 - iy;
-      const int e2 = mx * B1 + my;
-      if (e2 < e) continue;
-      Cx<T> p = cscale(Rb[e], sc), q = cscale(Rb[e2], sc);
-      Rb[e] = cx<T>((T)0.5 * (p.x + q.x), (T)0.5 * (p.y - q.y));
-      if (e2 != e) Rb[e2] = cx<T>((T)0.5 * (q.x + p.x), (T)0.5 * (q.y - p.y));
-    } else {
-      Rb[e] = cscale(Rb[e], sc);
-    }
-  }
-  __syncthreads();
-  // epilogue + fused RK4 stage update
-  const int64_t base = (int64_t)o * g.nh + (int64_t)kz * B0 * B1;
-  for (int e = threadIdx.x; e < B0 * B1; e += blockDim.x) {
-    Cx<T> r = Rb[e];
-    Cx<T> k;
-    if (O.mode == kEpiNegAdd) {
-      Cx<T> v = O.vt[(int64_t)kz * B0 * B1 + e];
-      k = cx<T>(-(v.x + r.x), -(v.y + r.y));
-    } else if (O.mode == kEpiNeg) {
-      k = cx<T>(-r.x, -r.y);
-    } else {
-      k = r;
-    }
-    const int64_t h = base + e;
-    if (a.kout) a.kout[h] = k;
-    if (a.rk_s) {
-      Cx<T> cc = a.cur[h], ac;
-      const int s = a.rk_s;
-      if (s == 1) {
-        ac = k;
-      } else {
-        ac = a.acc[h];
-        const T m = s < 4 ? (T)2 : (T)1;
-        ac = cx<T>(ac.x + m * k.x, ac.y + m * k.y);
-      }
-      if (s < 4) {
-        a.acc[h] = ac;
-        a.stage[h] = cx<T>(cc.x + a.cs * k.x, cc.y + a.cs * k.y);
-      } else {
-        a.cur[h] = cx<T>(cc.x + a.h6 * ac.x, cc.y + a.h6 * ac.y);
-      }
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// layout conversion: full block [comp][kx][ky][kz] <-> H layout [comp][kz][kx][ky]
-// ---------------------------------------------------------------------------
-template <typename T>
-__global__ void k_full_to_h(const Cx<T>* __restrict__ full, int ncomp, PadGeom g, Cx<T>* __restrict__ H) {
-  const int64_t total = g.nh * ncomp;
-  const int B0 = g.B[0], B1 = g.B[1], B2 = g.B[2];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i / g.nh);
-    int64_t r = i - c * g.nh;
-    const int iy = (int)(r % B1);
-    r /= B1;
-    const int ix = (int)(r % B0);
-    const int kz = (int)(r / B0);
-    H[i] = full[(int64_t)c * B0 * B1 * B2 + ((int64_t)ix * B1 + iy) * B2 + kz];
-  }
-}
-
-template <typename T>
-__global__ void k_h_to_full(const Cx<T>* __restrict__ H, int ncomp, PadGeom g, Cx<T>* __restrict__ full) {
-  const int B0 = g.B[0], B1 = g.B[1], B2 = g.B[2];
-  const int64_t nb = (int64_t)B0 * B1 * B2;
-  const int64_t total = nb * ncomp;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i / nb);
-    int64_t r = i - c * nb;
-    const int iz = (int)(r % B2);
-    r /= B2;
-    const int iy = (int)(r % B1);
-    const int ix = (int)(r / B1);
-    const Cx<T>* Hc = H + c * g.nh;
-    if (iz <= g.K[2]) {
-      full[i] = Hc[((int64_t)iz * B0 + ix) * B1 + iy];
-    } else {
-      const int kz = B2 - iz;  // -(iz - B2)
-      const int mx = ix == 0 ? 0 : B0 - ix, my = iy == 0 ? 0 : B1 - iy;
-      full[i] = cconj(Hc[((int64_t)kz * B0 + mx) * B1 + my]);
-    }
-  }
-}
-
+// launchers are instantiated per line length in blr_pad_L*.cu (parallel build)
+#define BLR_EXTERN_L(LL, A, B)                                                                         \
+  extern template void launch_xinv<double, WShape<A, B>>(blr_ctx*, PadEngine*, const XPassArgs<double>&); \
+  extern template void launch_xinv<float, WShape<A, B>>(blr_ctx*, PadEngine*, const XPassArgs<float>&);   \
+  extern template void launch_yinv<double, WShape<A, B>>(blr_ctx*, PadEngine*, const YPassArgs<double>&); \
+  extern template void launch_yinv<float, WShape<A, B>>(blr_ctx*, PadEngine*, const YPassArgs<float>&);   \
+  extern template void launch_yfwd<double, WShape<A, B>>(blr_ctx*, PadEngine*, const double2*, int, double2*); \
+  extern template void launch_yfwd<float, WShape<A, B>>(blr_ctx*, PadEngine*, const float2*, int, float2*);    \
+  extern template void launch_xfwd<double, WShape<A, B>>(blr_ctx*, PadEngine*, const FwdArgs<double>&);   \
+  extern template void launch_xfwd<float, WShape<A, B>>(blr_ctx*, PadEngine*, const FwdArgs<float>&);
+BLR_FOR_EACH_L(BLR_EXTERN_L)
+#undef BLR_EXTERN_L
+#define BLR_EXTERN_LZ(LL, A, B, OP)                                                                     \
+  extern template void launch_lines<double, WShape<A, B>, OP>(blr_ctx*, PadEngine*, const LineArgs<double>&); \
+  extern template void launch_lines<float, WShape<A, B>, OP>(blr_ctx*, PadEngine*, const LineArgs<float>&);
+#define BLR_EXTERN_L_ALLOPS(LL, A, B) \
+  BLR_EXTERN_LZ(LL, A, B, 0) BLR_EXTERN_LZ(LL, A, B, 1) BLR_EXTERN_LZ(LL, A, B, 2) BLR_EXTERN_LZ(LL, A, B, 3) \
+  BLR_EXTERN_LZ(LL, A, B, 4) BLR_EXTERN_LZ(LL, A, B, 5) BLR_EXTERN_LZ(LL, A, B, 6) BLR_EXTERN_LZ(LL, A, B, 7) \
+  BLR_EXTERN_LZ(LL, A, B, 8)
+BLR_FOR_EACH_LZ(BLR_EXTERN_L_ALLOPS)
+#undef BLR_EXTERN_L_ALLOPS
+#undef BLR_EXTERN_LZ
 // ---------------------------------------------------------------------------
 // host side: engine setup and launch helpers
 // ---------------------------------------------------------------------------
-struct PadEngine {
-  bool ok = false;
-  bool tried = false;
-  PadGeom g{};
-  double2* tw[3] = {nullptr, nullptr, nullptr};
-  size_t smem_inv = 0, smem_fwd = 0;
-  int line_smem_budget = 0;
-};
 
 static std::map<blr_ctx*, PadEngine>& engines() {
   static std::map<blr_ctx*, PadEngine> m;
@@ -555,21 +46,6 @@ void pad_engine_release(blr_ctx* c) {
   for (auto* p : it->second.tw)
     if (p) cudaFree(p);
   engines().erase(it);
-}
-
-template <typename T>
-static size_t inv_smem(const PadGeom& g) {
-  const int Pm = std::max(g.P[0], g.P[1]);
-  return sizeof(Cx<T>) * ((size_t)g.P[0] + g.P[1] + (size_t)g.B[1] * g.P[0] + 2 * (size_t)g.G * Pm);
-}
-template <typename T>
-static size_t fwd_smem(const PadGeom& g) {
-  return inv_smem<T>(g) + sizeof(Cx<T>) * (size_t)g.B[0] * g.B[1];
-}
-template <typename T>
-static size_t line_smem(const PadGeom& g, int Yt, int ns_blk, int no) {
-  return sizeof(Cx<T>) * ((size_t)g.P[2] + 2 * (size_t)Yt * g.P[2]) +
-         sizeof(T) * (size_t)(ns_blk + no) * Yt * g.P[2];
 }
 
 static int g_pad_disabled = -1;
@@ -586,26 +62,18 @@ static PadEngine* engine(blr_ctx* c) {
   if (g_pad_disabled) return nullptr;
   const Geom& gg = c->g;
   PadGeom& g = e.g;
-  bool ok0, ok1, ok2;
-  for (int a = 0; a < 3; ++a) { g.P[a] = gg.P[a]; g.K[a] = gg.K[a]; g.B[a] = gg.B[a]; }
-  g.fx = make_fft(g.P[0], &ok0);
-  g.fy = make_fft(g.P[1], &ok1);
-  g.fz = make_fft(g.P[2], &ok2);
-  if (!(ok0 && ok1 && ok2)) return nullptr;
+  for (int a = 0; a < 3; ++a) {
+    g.P[a] = gg.P[a]; g.K[a] = gg.K[a]; g.B[a] = gg.B[a];
+    if (!supported_len(g.P[a])) return nullptr;
+  }
   g.Kz1 = g.K[2] + 1;
   g.nh = (int64_t)g.Kz1 * g.B[0] * g.B[1];
   g.ns = (int64_t)g.Kz1 * g.P[0] * g.P[1];
+  g.n1 = (int64_t)g.Kz1 * g.B[1] * g.P[0];
   g.np = (int64_t)g.P[0] * g.P[1] * g.P[2];
   int dev;
   BLR_CUDA(cudaGetDevice(&dev));
-  int maxsm = 0;
-  BLR_CUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  g.G = 16;
-  while (g.G > 1 && fwd_smem<T>(g) > (size_t)maxsm) g.G /= 2;
-  if (fwd_smem<T>(g) > (size_t)maxsm) return nullptr;
-  e.smem_inv = inv_smem<T>(g);
-  e.smem_fwd = fwd_smem<T>(g);
-  e.line_smem_budget = std::min(maxsm, 110 * 1024);
+  BLR_CUDA(cudaDeviceGetAttribute(&e.line_smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   for (int a = 0; a < 3; ++a) {
     const int L = g.P[a];
     std::vector<double2> tw(L);
@@ -617,8 +85,6 @@ static PadEngine* engine(blr_ctx* c) {
     BLR_CUDA(cudaMalloc(&e.tw[a], L * sizeof(double2)));
     BLR_CUDA(cudaMemcpy(e.tw[a], tw.data(), L * sizeof(double2), cudaMemcpyHostToDevice));
   }
-  BLR_CUDA(cudaFuncSetAttribute(k_inv2d<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_inv));
-  BLR_CUDA(cudaFuncSetAttribute(k_fwd2d<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_fwd));
   e.ok = true;
   return &e;
 }
@@ -626,7 +92,53 @@ static PadEngine* engine(blr_ctx* c) {
 template <typename T>
 bool pad_engine_ok(blr_ctx* c) { return engine<T>(c) != nullptr; }
 
-// --- inverse 2-D ---------------------------------------------------------------
+template <typename T>
+static void dispatch_xinv(blr_ctx* c, PadEngine* e, const XPassArgs<T>& a) {
+  switch (e->g.P[0]) {
+#define X(LL, A, B) case LL: launch_xinv<T, WShape<A, B>>(c, e, a); break;
+    BLR_FOR_EACH_L(X)
+#undef X
+    default: throw Error(1, "unsupported pad length");
+  }
+}
+template <typename T>
+static void dispatch_yinv(blr_ctx* c, PadEngine* e, const YPassArgs<T>& a) {
+  switch (e->g.P[1]) {
+#define X(LL, A, B) case LL: launch_yinv<T, WShape<A, B>>(c, e, a); break;
+    BLR_FOR_EACH_L(X)
+#undef X
+    default: throw Error(1, "unsupported pad length");
+  }
+}
+template <typename T, int OP>
+static void dispatch_lines(blr_ctx* c, PadEngine* e, const LineArgs<T>& a) {
+  switch (e->g.P[2]) {
+#define X(LL, A, B) case LL: launch_lines<T, WShape<A, B>, OP>(c, e, a); break;
+    BLR_FOR_EACH_LZ(X)
+#undef X
+    default: throw Error(1, "unsupported pad length");
+  }
+}
+template <typename T>
+static void dispatch_yfwd(blr_ctx* c, PadEngine* e, const Cx<T>* in, int nf, Cx<T>* out) {
+  switch (e->g.P[1]) {
+#define X(LL, A, B) case LL: launch_yfwd<T, WShape<A, B>>(c, e, in, nf, out); break;
+    BLR_FOR_EACH_L(X)
+#undef X
+    default: throw Error(1, "unsupported pad length");
+  }
+}
+template <typename T>
+static void dispatch_xfwd(blr_ctx* c, PadEngine* e, const FwdArgs<T>& a) {
+  switch (e->g.P[0]) {
+#define X(LL, A, B) case LL: launch_xfwd<T, WShape<A, B>>(c, e, a); break;
+    BLR_FOR_EACH_L(X)
+#undef X
+    default: throw Error(1, "unsupported pad length");
+  }
+}
+
+// --- realization of band fields on the pad grid (x pass + y pass) ----------------
 template <typename T>
 struct InvSpec {
   const Cx<T>* src[3];
@@ -642,50 +154,86 @@ static InvSpec<T> inv1(const Cx<T>* src, int axis) {
   return s;
 }
 
+// S[f] = Y(X(field f)) for every spec; derivative multipliers: x before the
+// x pass, y / z before the y pass.
 template <typename T>
 static void inv2d(blr_ctx* c, PadEngine* e, const std::vector<InvSpec<T>>& f, Cx<T>* S) {
-  for (size_t off = 0; off < f.size(); off += kMaxInv) {
-    InvArgs<T> a;
-    std::memset(&a, 0, sizeof(a));
-    a.nf = (int)std::min<size_t>(kMaxInv, f.size() - off);
-    for (int i = 0; i < a.nf; ++i) {
-      const InvSpec<T>& s = f[off + i];
-      for (int t = 0; t < 3; ++t) { a.f[i].src[t] = s.src[t]; a.f[i].axis[t] = s.axis[t]; }
-      a.f[i].nterms = s.nterms;
+  const PadGeom& g = e->g;
+  std::vector<std::pair<const Cx<T>*, int>> xf;
+  std::vector<std::array<int, 3>> yx(f.size());
+  for (size_t i = 0; i < f.size(); ++i)
+    for (int t = 0; t < f[i].nterms; ++t) {
+      std::pair<const Cx<T>*, int> key(f[i].src[t], f[i].axis[t] == 0 ? 1 : 0);
+      int idx = -1;
+      for (size_t q = 0; q < xf.size(); ++q)
+        if (xf[q] == key) { idx = (int)q; break; }
+      if (idx < 0) { idx = (int)xf.size(); xf.push_back(key); }
+      yx[i][t] = idx;
     }
-    ProfScope ps(c, "pad_inv2d", (double)a.nf * (e->g.nh + e->g.ns) * sizeof(Cx<T>));
-    k_inv2d<T><<<a.nf * e->g.Kz1, 256, e->smem_inv, c->stream>>>(a, e->g, e->tw[0], e->tw[1],
-                                                                   S + (int64_t)off * e->g.ns);
-    BLR_LAUNCHED();
+  if ((int)xf.size() > kMaxX) throw Error(1, "too many x-pass fields");
+  Cx<T>* I = nullptr;
+  BLR_CUDA(cudaMallocAsync((void**)&I, xf.size() * g.n1 * sizeof(Cx<T>), c->stream));
+  {
+    XPassArgs<T> a;
+    std::memset(&a, 0, sizeof(a));
+    a.nx = (int)xf.size();
+    for (int i = 0; i < a.nx; ++i) { a.src[i] = xf[i].first; a.mulx[i] = xf[i].second; }
+    a.out = I;
+    ProfScope ps(c, "pad_xpass", (double)a.nx * (g.nh + g.n1) * sizeof(Cx<T>));
+    dispatch_xinv<T>(c, e, a);
+  }
+  for (size_t off = 0; off < f.size(); off += kMaxY) {
+    YPassArgs<T> a;
+    std::memset(&a, 0, sizeof(a));
+    a.ny = (int)std::min<size_t>(kMaxY, f.size() - off);
+    int nterm = 0;
+    for (int i = 0; i < a.ny; ++i) {
+      const InvSpec<T>& s = f[off + i];
+      a.nterms[i] = s.nterms;
+      for (int t = 0; t < 3; ++t) {
+        a.xf[i][t] = t < s.nterms ? yx[off + i][t] : 0;
+        a.axis[i][t] = (t < s.nterms && (s.axis[t] == 1 || s.axis[t] == 2)) ? s.axis[t] : -1;
+      }
+      nterm += s.nterms;
+    }
+    a.in = I;
+    a.out = S + (int64_t)off * g.ns;
+    ProfScope ps(c, "pad_ypass", ((double)nterm * g.n1 + a.ny * g.ns) * sizeof(Cx<T>));
+    dispatch_yinv<T>(c, e, a);
+  }
+  BLR_CUDA(cudaFreeAsync(I, c->stream));
+}
+
+// --- z lines -------------------------------------------------------------------------
+// ACC-op tables: output index / real-input index / sign per spectral field
+template <typename T>
+static void acc_tables(int op, LineArgs<T>& a) {
+  const int d = a.d, dd = d * d;
+  for (int f = 0; f < kMaxLineS; ++f) { a.oi[f] = 0; a.ri[f] = 0; a.sg[f] = 1.0; }
+  if (op == kOpMap || op == kOpMapTC) {
+    for (int f = 0; f < dd; ++f) {
+      a.oi[f] = f / d;
+      a.ri[f] = (op == kOpMap ? 0 : dd) + f % d;
+    }
+  } else if (op == kOpInvVol) {
+    for (int f = 0; f < dd; ++f) { a.oi[f] = f / d; a.ri[f] = f % d; }
+    for (int q = 0; q < d; ++q) { a.oi[dd + q] = d; a.ri[dd + q] = q; a.sg[dd + q] = -1.0; }
+    a.oi[dd + d] = d; a.ri[dd + d] = d; a.sg[dd + d] = -1.0;
+  } else if (op == kOpContract) {
+    for (int o = 0; o < 3; ++o)
+      for (int j = 0; j < 3; ++j) a.mi[o][j] = (o < d && j < d) ? (a.transpose ? j * d + o : o * d + j) : 0;
   }
 }
 
-// --- lines -------------------------------------------------------------------------
 template <typename T, int OP>
 static void lines(blr_ctx* c, PadEngine* e, LineArgs<T>& a, double bytes) {
-  PadGeom g = e->g;
-  const int ns_blk = OP == kOpContract ? a.d : a.ns;
-  const int no = OP == kOpRealize ? 0 : a.no;
-  int Yt = 16;
-  while (Yt > 1 && line_smem<T>(g, Yt, ns_blk, no) > (size_t)e->line_smem_budget) --Yt;
-  g.Yt = Yt;
-  const size_t smem = line_smem<T>(g, Yt, ns_blk, no);
-  static bool attr_set[2][16] = {};
-  bool& done = attr_set[sizeof(T) == 8 ? 0 : 1][OP];
-  if (!done) {
-    int dev, maxsm;
-    BLR_CUDA(cudaGetDevice(&dev));
-    BLR_CUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    BLR_CUDA(cudaFuncSetAttribute(k_lines<T, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
-    done = true;
-  }
-  const int nyc = (g.P[1] + Yt - 1) / Yt;
-  ProfScope ps(c, "pad_lines", bytes);
-  k_lines<T, OP><<<g.P[0] * nyc, 256, smem, c->stream>>>(a, g, e->tw[2]);
-  BLR_LAUNCHED();
+  a.op = OP;
+  acc_tables<T>(OP, a);
+  ProfScope ps(c, "pad_zlines", bytes);
+  dispatch_lines<T, OP>(c, e, a);
 }
 
-// --- forward 2-D ---------------------------------------------------------------------
+// --- projection back to the band (y pass + x pass + fix-up) ------------------------
 template <typename T>
 struct FwdSpec {
   const Cx<T>* sin[3];
@@ -713,9 +261,35 @@ struct Rk {
   void* stage = nullptr;
 };
 
+// kout / RK4 component index = output index
 template <typename T>
 static void fwd2d(blr_ctx* c, PadEngine* e, const std::vector<FwdSpec<T>>& outs, Cx<T>* kout, const Rk& rk) {
-  // chunks must keep the state/kout component index = output index
+  const PadGeom& g = e->g;
+  std::vector<const Cx<T>*> sf;
+  std::vector<std::array<int, 3>> fi(outs.size());
+  for (size_t i = 0; i < outs.size(); ++i)
+    for (int t = 0; t < outs[i].nterms; ++t) {
+      int idx = -1;
+      for (size_t q = 0; q < sf.size(); ++q)
+        if (sf[q] == outs[i].sin[t]) { idx = (int)q; break; }
+      if (idx < 0) { idx = (int)sf.size(); sf.push_back(outs[i].sin[t]); }
+      fi[i][t] = idx;
+    }
+  Cx<T>* I = nullptr;
+  BLR_CUDA(cudaMallocAsync((void**)&I, sf.size() * g.n1 * sizeof(Cx<T>), c->stream));
+  {
+    size_t i = 0;
+    while (i < sf.size()) {
+      size_t j = i + 1;
+      while (j < sf.size() && sf[j] == sf[i] + (int64_t)(j - i) * g.ns) ++j;
+      const int nf = (int)(j - i);
+      ProfScope ps(c, "pad_ypass_fwd", (double)nf * (g.ns + g.n1) * sizeof(Cx<T>));
+      dispatch_yfwd<T>(c, e, sf[i], nf, I + (int64_t)i * g.n1);
+      i = j;
+    }
+  }
+  Cx<T>* z0 = nullptr;
+  BLR_CUDA(cudaMallocAsync((void**)&z0, outs.size() * (size_t)g.B[0] * g.B[1] * sizeof(Cx<T>), c->stream));
   for (size_t off = 0; off < outs.size(); off += kMaxFwd) {
     FwdArgs<T> a;
     std::memset(&a, 0, sizeof(a));
@@ -723,14 +297,19 @@ static void fwd2d(blr_ctx* c, PadEngine* e, const std::vector<FwdSpec<T>>& outs,
     int nterm = 0;
     for (int i = 0; i < a.no; ++i) {
       const FwdSpec<T>& s = outs[off + i];
-      for (int t = 0; t < 3; ++t) { a.o[i].sin[t] = s.sin[t]; a.o[i].axis[t] = s.axis[t]; }
+      for (int t = 0; t < 3; ++t) {
+        a.o[i].f[t] = t < s.nterms ? fi[off + i][t] : 0;
+        a.o[i].axis[t] = s.axis[t];
+      }
       a.o[i].nterms = s.nterms;
       a.o[i].mode = s.mode;
       a.o[i].vt = s.vt;
       nterm += s.nterms;
     }
-    a.scale = (T)(1.0 / (double)e->g.np);
-    const int64_t shift = (int64_t)off * e->g.nh;
+    a.in = I;
+    a.scale = (T)(1.0 / (double)g.np);
+    a.z0 = z0 + (int64_t)off * g.B[0] * g.B[1];
+    const int64_t shift = (int64_t)off * g.nh;
     a.kout = kout ? kout + shift : nullptr;
     a.rk_s = rk.s;
     a.cs = (T)rk.cs;
@@ -738,11 +317,16 @@ static void fwd2d(blr_ctx* c, PadEngine* e, const std::vector<FwdSpec<T>>& outs,
     a.cur = rk.cur ? (Cx<T>*)rk.cur + shift : nullptr;
     a.acc = rk.acc ? (Cx<T>*)rk.acc + shift : nullptr;
     a.stage = rk.stage ? (Cx<T>*)rk.stage + shift : nullptr;
-    ProfScope ps(c, "pad_fwd2d",
-                 ((double)nterm * e->g.ns + a.no * e->g.nh * (rk.s ? 4 : 2)) * sizeof(Cx<T>));
-    k_fwd2d<T><<<a.no * e->g.Kz1, 256, e->smem_fwd, c->stream>>>(a, e->g, e->tw[0], e->tw[1]);
+    {
+      ProfScope ps(c, "pad_xpass_fwd", ((double)nterm * g.n1 + a.no * g.nh * (rk.s ? 4 : 2)) * sizeof(Cx<T>));
+      dispatch_xfwd<T>(c, e, a);
+    }
+    const int64_t n0 = (int64_t)a.no * g.B[0] * g.B[1];
+    k_fix0<T><<<grid_blocks(n0, 256), 256, 0, c->stream>>>(a, g);
     BLR_LAUNCHED();
   }
+  BLR_CUDA(cudaFreeAsync(z0, c->stream));
+  BLR_CUDA(cudaFreeAsync(I, c->stream));
 }
 
 template <typename T>

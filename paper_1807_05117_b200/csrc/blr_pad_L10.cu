@@ -1,0 +1,32 @@
+// blr_pad_L10.cu — explicit instantiation of the pad-engine launchers for
+// line length 10 = 5 x 2 (one translation unit per length: parallel build).
+#include "blr_pad_kernels.cuh"
+
+namespace blr {
+template void launch_xinv<double, WShape<5, 2>>(blr_ctx*, PadEngine*, const XPassArgs<double>&);
+template void launch_yinv<double, WShape<5, 2>>(blr_ctx*, PadEngine*, const YPassArgs<double>&);
+template void launch_yfwd<double, WShape<5, 2>>(blr_ctx*, PadEngine*, const double2*, int, double2*);
+template void launch_xfwd<double, WShape<5, 2>>(blr_ctx*, PadEngine*, const FwdArgs<double>&);
+template void launch_lines<double, WShape<5, 2>, 0>(blr_ctx*, PadEngine*, const LineArgs<double>&);
+template void launch_lines<double, WShape<5, 2>, 1>(blr_ctx*, PadEngine*, const LineArgs<double>&);
+template void launch_lines<double, WShape<5, 2>, 2>(blr_ctx*, PadEngine*, const LineArgs<double>&);
+template void launch_lines<double, WShape<5, 2>, 3>(blr_ctx*, PadEngine*, const LineArgs<double>&);
+template void launch_lines<double, WShape<5, 2>, 4>(blr_ctx*, PadEngine*, const LineArgs<double>&);
+template void launch_lines<double, WShape<5, 2>, 5>(blr_ctx*, PadEngine*, const LineArgs<double>&);
+template void launch_lines<double, WShape<5, 2>, 6>(blr_ctx*, PadEngine*, const LineArgs<double>&);
+template void launch_lines<double, WShape<5, 2>, 7>(blr_ctx*, PadEngine*, const LineArgs<double>&);
+template void launch_lines<double, WShape<5, 2>, 8>(blr_ctx*, PadEngine*, const LineArgs<double>&);
+template void launch_xinv<float, WShape<5, 2>>(blr_ctx*, PadEngine*, const XPassArgs<float>&);
+template void launch_yinv<float, WShape<5, 2>>(blr_ctx*, PadEngine*, const YPassArgs<float>&);
+template void launch_yfwd<float, WShape<5, 2>>(blr_ctx*, PadEngine*, const float2*, int, float2*);
+template void launch_xfwd<float, WShape<5, 2>>(blr_ctx*, PadEngine*, const FwdArgs<float>&);
+template void launch_lines<float, WShape<5, 2>, 0>(blr_ctx*, PadEngine*, const LineArgs<float>&);
+template void launch_lines<float, WShape<5, 2>, 1>(blr_ctx*, PadEngine*, const LineArgs<float>&);
+template void launch_lines<float, WShape<5, 2>, 2>(blr_ctx*, PadEngine*, const LineArgs<float>&);
+template void launch_lines<float, WShape<5, 2>, 3>(blr_ctx*, PadEngine*, const LineArgs<float>&);
+template void launch_lines<float, WShape<5, 2>, 4>(blr_ctx*, PadEngine*, const LineArgs<float>&);
+template void launch_lines<float, WShape<5, 2>, 5>(blr_ctx*, PadEngine*, const LineArgs<float>&);
+template void launch_lines<float, WShape<5, 2>, 6>(blr_ctx*, PadEngine*, const LineArgs<float>&);
+template void launch_lines<float, WShape<5, 2>, 7>(blr_ctx*, PadEngine*, const LineArgs<float>&);
+template void launch_lines<float, WShape<5, 2>, 8>(blr_ctx*, PadEngine*, const LineArgs<float>&);
+}  // namespace blr

@@ -1,0 +1,32 @@
+// blr_pad_L40.cu — explicit instantiation of the pad-engine launchers for
+// line length 40 = 8 x 5 (one translation unit per length: parallel build).
+#include "blr_pad_kernels.cuh"
+
+namespace blr {
+template void launch_xinv<double, WShape<8, 5>>(blr_ctx*, PadEngine*, const XPassArgs<double>&);
+template void launch_yinv<double, WShape<8, 5>>(blr_ctx*, PadEngine*, const YPassArgs<double>&);
+template void launch_yfwd<double, WShape<8, 5>>(blr_ctx*, PadEngine*, const double2*, int, double2*);
+template void launch_xfwd<double, WShape<8, 5>>(blr_ctx*, PadEngine*, const FwdArgs<double>&);
+template void launch_lines<double, WShape<8, 5>, 0>(blr_ctx*, PadEngine*, const LineArgs<double>&);
+template void launch_lines<double, WShape<8, 5>, 1>(blr_ctx*, PadEngine*, const LineArgs<double>&);
+template void launch_lines<double, WShape<8, 5>, 2>(blr_ctx*, PadEngine*, const LineArgs<double>&);
+template void launch_lines<double, WShape<8, 5>, 3>(blr_ctx*, PadEngine*, const LineArgs<double>&);
+template void launch_lines<double, WShape<8, 5>, 4>(blr_ctx*, PadEngine*, const LineArgs<double>&);
+template void launch_lines<double, WShape<8, 5>, 5>(blr_ctx*, PadEngine*, const LineArgs<double>&);
+template void launch_lines<double, WShape<8, 5>, 6>(blr_ctx*, PadEngine*, const LineArgs<double>&);
+template void launch_lines<double, WShape<8, 5>, 7>(blr_ctx*, PadEngine*, const LineArgs<double>&);
+template void launch_lines<double, WShape<8, 5>, 8>(blr_ctx*, PadEngine*, const LineArgs<double>&);
+template void launch_xinv<float, WShape<8, 5>>(blr_ctx*, PadEngine*, const XPassArgs<float>&);
+template void launch_yinv<float, WShape<8, 5>>(blr_ctx*, PadEngine*, const YPassArgs<float>&);
+template void launch_yfwd<float, WShape<8, 5>>(blr_ctx*, PadEngine*, const float2*, int, float2*);
+template void launch_xfwd<float, WShape<8, 5>>(blr_ctx*, PadEngine*, const FwdArgs<float>&);
+template void launch_lines<float, WShape<8, 5>, 0>(blr_ctx*, PadEngine*, const LineArgs<float>&);
+template void launch_lines<float, WShape<8, 5>, 1>(blr_ctx*, PadEngine*, const LineArgs<float>&);
+template void launch_lines<float, WShape<8, 5>, 2>(blr_ctx*, PadEngine*, const LineArgs<float>&);
+template void launch_lines<float, WShape<8, 5>, 3>(blr_ctx*, PadEngine*, const LineArgs<float>&);
+template void launch_lines<float, WShape<8, 5>, 4>(blr_ctx*, PadEngine*, const LineArgs<float>&);
+template void launch_lines<float, WShape<8, 5>, 5>(blr_ctx*, PadEngine*, const LineArgs<float>&);
+template void launch_lines<float, WShape<8, 5>, 6>(blr_ctx*, PadEngine*, const LineArgs<float>&);
+template void launch_lines<float, WShape<8, 5>, 7>(blr_ctx*, PadEngine*, const LineArgs<float>&);
+template void launch_lines<float, WShape<8, 5>, 8>(blr_ctx*, PadEngine*, const LineArgs<float>&);
+}  // namespace blr

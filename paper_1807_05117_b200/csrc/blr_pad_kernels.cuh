@@ -1,0 +1,745 @@
+// blr_pad.cu — the fused pad-grid engine for every truncated convolution on
+// the hot path (transport.py:206-303, deformation.py:63-72).  No cuFFT and no
+// zero-padded grids: a right-hand side is a chain of batched 1-D transforms
+// with the data movement fused in,
+//
+//   k_xinv    band H [kz][kx][ky] -> inverse x FFT (x derivative multiplier,
+//             zero padding fused) -> I [f][kz][ky][x]
+//   k_yinv    -> inverse y FFT (y / z multipliers, sums of terms fused)
+//             -> S [f][kz][x][y]        (only kz = 0..K: Hermitian half)
+//   k_lines   per z-line: C2R (two real lines per complex FFT), the RHS
+//             pointwise product streamed into per-output accumulators (reading
+//             cached real pad fields), R2C back to S (kz = 0..K)
+//   k_yfwd    forward y FFT, band ky kept -> I
+//   k_xfwd    forward x FFT, band kx kept, post-transform multipliers (flux
+//             divergence), 1/P^3, -(v + .) / negation, fused RK4 stage update
+//   k_fix0    the kz = 0 plane: Hermitian symmetrization + the same epilogue
+//
+// Band state lives in the "H layout" [comp][kz 0..K][kx][ky] (Hermitian half);
+// node records are converted back to the reference's full blocks.
+#pragma once
+
+#include "blr_fft.cuh"
+#include "blr_internal.cuh"
+
+#include <cuda_pipeline_primitives.h>
+
+#include <cmath>
+#include <array>
+#include <cstring>
+
+namespace blr {
+
+// ---------------------------------------------------------------------------
+// geometry
+// ---------------------------------------------------------------------------
+struct PadGeom {
+  int P[3], K[3], B[3];
+  int Kz1;       // K[2] + 1
+  int64_t nh;    // H-layout component size Kz1*B0*B1
+  int64_t ns;    // S-layout field size Kz1*P0*P1
+  int64_t n1;    // I-layout field size Kz1*B1*P0
+  int64_t np;    // real pad field size
+};
+
+constexpr int kWarps = 8;  // warps per CTA in the x / y pass kernels
+
+__device__ __forceinline__ int bin_to_index(int p, int P, int K, int B) {
+  if (p <= K) return p;
+  if (p >= P - K) return p - P + B;
+  return -1;
+}
+
+template <typename T>
+__device__ __forceinline__ void load_tw(Cx<T>* dst, const double2* src, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = cx<T>((T)src[i].x, (T)src[i].y);
+}
+
+template <typename T>
+__device__ __forceinline__ Cx<T> mul_ik(Cx<T> z, T k) { return cx<T>(-(k * z.y), k * z.x); }
+
+// ---------------------------------------------------------------------------
+// inverse x pass: band H [kz][kx][ky] -> I [xf][kz][ky][x]
+// ---------------------------------------------------------------------------
+constexpr int kMaxX = 40;
+constexpr int kMaxY = 32;
+
+template <typename T>
+struct XPassArgs {
+  const Cx<T>* src[kMaxX];
+  int mulx[kMaxX];
+  int nx;
+  Cx<T>* out;
+};
+
+template <typename T, class S>
+__global__ void __launch_bounds__(kWarps * 32) k_xinv(XPassArgs<T> a, PadGeom g, const double2* __restrict__ twg) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Cx<T>* tw = (Cx<T>*)smem_raw;
+  Cx<T>* tile = tw + S::L + (threadIdx.x >> 5) * S::TILE;
+  constexpr int LPC = kWarps * S::LPW;
+  const int nyb = (g.B[1] + LPC - 1) / LPC;
+  const int per = g.Kz1 * nyb;
+  const int xf = blockIdx.x / per;
+  const int r = blockIdx.x - xf * per;
+  const int kz = r / nyb;
+  const int ky0 = (r - kz * nyb) * LPC + (threadIdx.x >> 5) * S::LPW;
+  load_tw<T>(tw, twg, S::L);
+  __syncthreads();
+  const int nl = min(S::LPW, g.B[1] - ky0);
+  if (nl <= 0) return;
+  const int K0 = g.K[0], B0 = g.B[0], B1 = g.B[1];
+  const Cx<T>* src = a.src[xf] + ((int64_t)kz * B0) * B1 + ky0;
+  const bool mulx = a.mulx[xf] != 0;
+  Cx<T>* out = a.out + xf * g.n1 + ((int64_t)kz * B1 + ky0) * S::L;
+  auto load = [&](int line, int p) -> Cx<T> {
+    const int ix = bin_to_index(p, S::L, K0, B0);
+    if (ix < 0) return cx<T>(0, 0);
+    Cx<T> z = src[ix * B1 + line];
+    if (mulx) z = mul_ik<T>(z, (T)(kTwoPi * (double)freq_of(ix, K0, B0)));
+    return z;
+  };
+  auto store = [&](int line, int x, int, Cx<T> v) { out[line * S::L + x] = v; };
+  wfft<T, S, true>(tile, tw, nl, load, store);
+}
+
+// ---------------------------------------------------------------------------
+// inverse y pass: I [xf][kz][ky][x] -> S [yf][kz][x][y]
+// ---------------------------------------------------------------------------
+template <typename T>
+struct YPassArgs {
+  int xf[kMaxY][3];
+  int axis[kMaxY][3];  // pre-multiplier: -1, 1 (i ky), 2 (i kz)
+  int nterms[kMaxY];
+  int ny;
+  const Cx<T>* in;
+  Cx<T>* out;
+};
+
+template <typename T, class S>
+__global__ void __launch_bounds__(kWarps * 32) k_yinv(YPassArgs<T> a, PadGeom g, const double2* __restrict__ twg) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Cx<T>* tw = (Cx<T>*)smem_raw;
+  Cx<T>* tile = tw + S::L + (threadIdx.x >> 5) * S::TILE;
+  constexpr int LPC = kWarps * S::LPW;
+  const int P0 = g.P[0], K1 = g.K[1], B1 = g.B[1];
+  const int nxb = (P0 + LPC - 1) / LPC;
+  const int per = g.Kz1 * nxb;
+  const int yf = blockIdx.x / per;
+  const int r = blockIdx.x - yf * per;
+  const int kz = r / nxb;
+  const int x0 = (r - kz * nxb) * LPC + (threadIdx.x >> 5) * S::LPW;
+  load_tw<T>(tw, twg, S::L);
+  __syncthreads();
+  const int nl = min(S::LPW, P0 - x0);
+  if (nl <= 0) return;
+  const int nt = a.nterms[yf];
+  const Cx<T>* src[3];
+  int ax[3];
+  for (int t = 0; t < 3; ++t) {
+    src[t] = t < nt ? a.in + a.xf[yf][t] * g.n1 + (int64_t)kz * B1 * P0 + x0 : nullptr;
+    ax[t] = a.axis[yf][t];
+  }
+  const T kzk = (T)(kTwoPi * (double)kz);
+  Cx<T>* out = a.out + yf * g.ns + ((int64_t)kz * P0 + x0) * S::L;
+  auto load = [&](int line, int q) -> Cx<T> {
+    const int iy = bin_to_index(q, S::L, K1, B1);
+    Cx<T> acc = cx<T>(0, 0);
+    if (iy < 0) return acc;
+    for (int t = 0; t < nt; ++t) {
+      Cx<T> z = src[t][iy * P0 + line];
+      if (ax[t] == 1) z = mul_ik<T>(z, (T)(kTwoPi * (double)freq_of(iy, K1, B1)));
+      else if (ax[t] == 2) z = mul_ik<T>(z, kzk);
+      acc = cadd(acc, z);
+    }
+    return acc;
+  };
+  auto store = [&](int line, int y, int, Cx<T> v) { out[line * S::L + y] = v; };
+  wfft<T, S, true>(tile, tw, nl, load, store);
+}
+
+// ---------------------------------------------------------------------------
+// z lines: C2R of the spectral inputs (two per complex FFT), streaming
+// pointwise products into per-output accumulators, R2C of the outputs
+// ---------------------------------------------------------------------------
+enum LineOp {
+  kOpRealize = 0,   // write realized inputs (wout) only
+  kOpMap = 1,       // out_i = sum_j S[ij] V_j                 (+ wout cache of S)
+  kOpMapTC = 2,     // out_i = sum_j S[ij] V_j + sum_j Du_ij dV_j   (Du, V, dV real)
+  kOpMapTF = 3,     // out = [Du.V | dDu.V + Du.dV]            (Du, dDu spectral)
+  kOpInvVol = 4,    // out = [Dw.V | -V.G - J Dv]
+  kOpBwdVol = 5,    // out = [Dw.V | dDw.V + Dw.dV | vol | vol tangent]
+  kOpOuter = 6,     // out_ij = rho_i V_j
+  kOpOuterPair = 7, // out = [rho x V | drho x V + rho x dV]
+  kOpContract = 8,  // out_i = sum_n w_n sum_j M_n(ji|ij) rho_n,j   (M real, cached)
+};
+
+constexpr int kMaxLineS = 28;
+constexpr int kMaxLineR = 16;
+constexpr int kMaxLineO = 18;
+
+template <typename T>
+struct LineArgs {
+  const Cx<T>* sin[kMaxLineS];
+  const T* rin[kMaxLineR];
+  Cx<T>* sout[kMaxLineO];
+  T* wout[kMaxLineS];
+  int op;
+  int ns, nr, no;
+  int d;
+  int n_nodes;
+  int64_t sin_node_stride;  // complex entries between nodes (per input field)
+  int64_t rin_node_stride;  // real entries between nodes
+  double w[32];
+  int transpose;
+  // ACC-op tables (host-built): output index, real-input index and sign per field
+  int oi[kMaxLineS], ri[kMaxLineS];
+  double sg[kMaxLineS];
+  int mi[3][3];  // contraction: rin index of M(o, j)
+};
+
+// Per-op compile-time traits of the z-line kernel.
+//   ACC ops: every realized spectral input adds sign * s * R[ri] to output
+//            oi (or, for the contraction, d terms); outputs live in registers.
+//   REAL ops: realized inputs are kept in shared memory and the outputs are
+//            formed on the fly while loading the R2C.
+template <int OP> struct ZOp {
+  static constexpr bool acc = OP == kOpMap || OP == kOpMapTC || OP == kOpInvVol || OP == kOpContract;
+  static constexpr int nomax = OP == kOpInvVol ? 4 : 3;
+};
+
+constexpr int kZWarps = 4;
+
+template <typename T, class S, int OP>
+__device__ __forceinline__ T z_output(const LineArgs<T>& a, const T* Rsm, int ldR, int li, int64_t gi, int o) {
+  const int d = a.d, dd = d * d;
+  auto Rr = [&](int q) { return __ldg(a.rin[q] + gi); };
+  auto Sm = [&](int f) { return Rsm[f * ldR + li]; };
+  if constexpr (OP == kOpOuter) {
+    const int i = o / d, j = o - i * d;
+    return Sm(i) * Rr(j);
+  } else if constexpr (OP == kOpOuterPair) {
+    if (o < dd) {
+      const int i = o / d, j = o - i * d;
+      return Sm(i) * Rr(j);
+    }
+    const int q = o - dd, i = q / d, j = q - i * d;
+    return Sm(d + i) * Rr(j) + Sm(i) * Rr(d + j);
+  } else if constexpr (OP == kOpMapTF) {
+    if (o < d) {
+      T b = 0;
+      for (int j = 0; j < d; ++j) b += Sm(o * d + j) * Rr(j);
+      return b;
+    }
+    const int i = o - d;
+    T a1 = 0, a2 = 0;
+    for (int j = 0; j < d; ++j) a1 += Sm(dd + i * d + j) * Rr(j);
+    for (int j = 0; j < d; ++j) a2 += Sm(i * d + j) * Rr(d + j);
+    return a1 + a2;
+  } else if constexpr (OP == kOpBwdVol) {
+    // S: Dw [0,dd) dDw [dd,2dd) G [2dd,+d) dG [2dd+d,+d) J dJ ; R: V, dV, Dv, dDv
+    if (o < d) {
+      T b = 0;
+      for (int j = 0; j < d; ++j) b += Sm(o * d + j) * Rr(j);
+      return b;
+    }
+    if (o < 2 * d) {
+      const int i = o - d;
+      T a1 = 0, a2 = 0;
+      for (int j = 0; j < d; ++j) a1 += Sm(dd + i * d + j) * Rr(j);
+      for (int j = 0; j < d; ++j) a2 += Sm(i * d + j) * Rr(d + j);
+      return a1 + a2;
+    }
+    const int g0 = 2 * dd, dg0 = 2 * dd + d, jj = 2 * dd + 2 * d;
+    if (o == 2 * d) {
+      T s = 0;
+      for (int q = 0; q < d; ++q) s += Rr(q) * Sm(g0 + q);
+      return -s - Sm(jj) * Rr(2 * d);
+    }
+    T s1 = 0, s2 = 0;
+    for (int q = 0; q < d; ++q) s1 += Rr(d + q) * Sm(g0 + q);
+    for (int q = 0; q < d; ++q) s2 += Rr(q) * Sm(dg0 + q);
+    return -s1 - s2 - Sm(jj + 1) * Rr(2 * d) - Sm(jj) * Rr(2 * d + 1);
+  }
+  return 0;
+}
+
+// z lines: per warp LPW lines (x fixed, consecutive y).  Spectral inputs are
+// prefetched pair by pair with cp.async (double buffered), C2R'd two per
+// complex FFT, combined with the cached real pad fields, R2C'd back.
+template <typename T, class S, int OP>
+__global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom g, const double2* __restrict__ twz_g) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  using Tr = ZOp<OP>;
+  constexpr int L = S::L;
+  constexpr int NOM = Tr::nomax;
+  const int P0 = g.P[0], P1 = g.P[1], K2 = g.K[2], Kz1 = g.Kz1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int LPC = kZWarps * S::LPW;
+  const int nyc = (P1 + LPC - 1) / LPC;
+  const int x = blockIdx.x / nyc;
+  const int y0 = (blockIdx.x - x * nyc) * LPC + warp * S::LPW;
+  const int ns_blk = OP == kOpContract ? a.d : a.ns;
+  const int nreal = (Tr::acc || OP == kOpRealize) ? 0 : ns_blk;
+  // shared layout: tw | per warp { tile | stage[2][2][Kz1*LPW] | xbuf[LPW*L] | Rsm[nreal][LPW*L] }
+  const int stage_n = 2 * 2 * Kz1 * S::LPW;
+  const size_t warp_bytes =
+      sizeof(Cx<T>) * ((size_t)S::TILE + stage_n + (size_t)S::LPW * L) + sizeof(T) * (size_t)nreal * S::LPW * L;
+  Cx<T>* tw = (Cx<T>*)smem_raw;
+  unsigned char* wb = smem_raw + sizeof(Cx<T>) * L + warp * warp_bytes;
+  Cx<T>* tile = (Cx<T>*)wb;
+  Cx<T>* stage = tile + S::TILE;
+  Cx<T>* xbuf = stage + stage_n;
+  T* Rsm = (T*)(xbuf + S::LPW * L);
+  const int ldR = S::LPW * L;
+  load_tw<T>(tw, twz_g, L);
+  __syncthreads();
+  const int nl = min(S::LPW, P1 - y0);
+  if (nl <= 0) return;
+  const int64_t sline = (int64_t)x * P1 + y0;
+  const int64_t kzs = (int64_t)P0 * P1;
+  const int64_t rline = ((int64_t)x * P1 + y0) * L;
+  // step-B ownership: lane (bl, k1) owns z = k1 + R1*k2
+  const int bl = lane / S::R1, k1 = lane - (lane / S::R1) * S::R1;
+  const bool own = bl < nl && bl < S::LPW;
+  T acc[NOM][S::R2];
+#pragma unroll
+  for (int o = 0; o < NOM; ++o)
+#pragma unroll
+    for (int k2 = 0; k2 < S::R2; ++k2) acc[o][k2] = 0;
+  if constexpr (OP == kOpMapTC) {
+    // acc_i = sum_j Du_ij dV_j  (rin: Du [0,dd) V [dd,dd+d) dV [dd+d, dd+2d))
+    if (own) {
+      const int d = a.d, dd = d * d;
+#pragma unroll
+      for (int k2 = 0; k2 < S::R2; ++k2) {
+        const int64_t gi = rline + bl * L + k1 + S::R1 * k2;
+#pragma unroll
+        for (int o = 0; o < NOM; ++o) {
+          if (o < d) {
+            T s = 0;
+            for (int j = 0; j < d; ++j) s += __ldg(a.rin[o * d + j] + gi) * __ldg(a.rin[dd + d + j] + gi);
+            acc[o][k2] = s;
+          }
+        }
+      }
+    }
+  }
+  const int npair = (ns_blk + 1) / 2;
+  const int nloop = OP == kOpContract ? a.n_nodes : 1;
+  const int total = nloop * npair;
+  // prefetch spectra of pair index q (node-major) into stage buffer q & 1
+  auto prefetch = [&](int q) {
+    const int node = q / npair, p = q - node * npair;
+    const int64_t noff = OP == kOpContract ? node * a.sin_node_stride : 0;
+    Cx<T>* st = stage + (q & 1) * 2 * Kz1 * S::LPW;
+    for (int ff = 0; ff < 2; ++ff) {
+      const int f = 2 * p + ff;
+      if (f >= ns_blk) break;
+      const Cx<T>* src = a.sin[f] + noff + sline;
+      for (int i = lane; i < Kz1 * nl; i += 32) {
+        const int k = i / nl, l = i - (i / nl) * nl;
+        __pipeline_memcpy_async(st + ff * Kz1 * S::LPW + k * S::LPW + l, src + k * kzs + l, sizeof(Cx<T>));
+      }
+    }
+    __pipeline_commit();
+  };
+  prefetch(0);
+  for (int q = 0; q < total; ++q) {
+    if (q + 1 < total) {
+      prefetch(q + 1);
+      __pipeline_wait_prior(1);
+    } else {
+      __pipeline_wait_prior(0);
+    }
+    __syncwarp();
+    const int node = q / npair, p = q - node * npair;
+    const int f = 2 * p;
+    const bool two = f + 1 < ns_blk;
+    const Cx<T>* st1 = stage + (q & 1) * 2 * Kz1 * S::LPW;
+    const Cx<T>* st2 = st1 + Kz1 * S::LPW;
+    auto load = [&](int line, int k) -> Cx<T> {
+      if (k == 0) return cx<T>(st1[line].x, two ? st2[line].x : (T)0);
+      if (k <= K2) {
+        const Cx<T> F1 = st1[k * S::LPW + line];
+        const Cx<T> F2 = two ? st2[k * S::LPW + line] : cx<T>(0, 0);
+        return cx<T>(F1.x - F2.y, F1.y + F2.x);
+      }
+      if (k >= L - K2) {
+        const int kk = L - k;
+        const Cx<T> F1 = st1[kk * S::LPW + line];
+        const Cx<T> F2 = two ? st2[kk * S::LPW + line] : cx<T>(0, 0);
+        return cx<T>(F1.x + F2.y, F2.x - F1.y);
+      }
+      return cx<T>(0, 0);
+    };
+    auto store = [&](int line, int z, int k2, Cx<T> v) {
+      const int li = line * L + z;
+      const int64_t gi = rline + li;
+      if constexpr (OP == kOpRealize) {
+        a.wout[f][gi] = v.x;
+        if (two) a.wout[f + 1][gi] = v.y;
+      } else if constexpr (!Tr::acc) {
+        Rsm[f * ldR + li] = v.x;
+        if (two) Rsm[(f + 1) * ldR + li] = v.y;
+      } else if constexpr (OP == kOpContract) {
+        const T wn = (T)a.w[node];
+        const int64_t go = gi + node * a.rin_node_stride;
+#pragma unroll
+        for (int o = 0; o < NOM; ++o) {
+          if (o < a.d) {
+            const T m1 = __ldg(a.rin[a.mi[o][f]] + go);
+            T c = m1 * v.x;
+            if (two) c += __ldg(a.rin[a.mi[o][f + 1]] + go) * v.y;
+            acc[o][k2] += wn * c;
+          }
+        }
+      } else {
+        if (OP == kOpMap && a.wout[f]) {
+          a.wout[f][gi] = v.x;
+          if (two) a.wout[f + 1][gi] = v.y;
+        }
+        const int o1 = a.oi[f], o2 = two ? a.oi[f + 1] : -1;
+        const T c1 = a.sg[f] * v.x * __ldg(a.rin[a.ri[f]] + gi);
+        const T c2 = two ? a.sg[f + 1] * v.y * __ldg(a.rin[a.ri[f + 1]] + gi) : (T)0;
+#pragma unroll
+        for (int o = 0; o < NOM; ++o) {
+          if (o == o1) acc[o][k2] += c1;
+          if (o == o2) acc[o][k2] += c2;
+        }
+      }
+    };
+    wfft<T, S, true>(tile, tw, nl, load, store);
+  }
+  if constexpr (OP == kOpRealize) return;
+  const int no = a.no;
+  for (int o = 0; o < no; o += 2) {
+    const bool two = o + 1 < no;
+    if constexpr (Tr::acc) {
+      if (own) {
+#pragma unroll
+        for (int k2 = 0; k2 < S::R2; ++k2) {
+          T v1 = 0, v2 = 0;
+#pragma unroll
+          for (int q = 0; q < NOM; ++q) {
+            if (q == o) v1 = acc[q][k2];
+            if (q == o + 1) v2 = acc[q][k2];
+          }
+          xbuf[bl * L + k1 + S::R1 * k2] = cx<T>(v1, v2);
+        }
+      }
+      __syncwarp();
+    }
+    auto load = [&](int line, int z) -> Cx<T> {
+      if constexpr (Tr::acc) {
+        return xbuf[line * L + z];
+      } else {
+        const int li = line * L + z;
+        const int64_t gi = rline + li;
+        return cx<T>(z_output<T, S, OP>(a, Rsm, ldR, li, gi, o),
+                     two ? z_output<T, S, OP>(a, Rsm, ldR, li, gi, o + 1) : (T)0);
+      }
+    };
+    auto store = [&](int line, int k, int, Cx<T> v) { xbuf[line * L + k] = v; };
+    wfft<T, S, false>(tile, tw, nl, load, store);
+    Cx<T>* O1 = a.sout[o] + sline;
+    Cx<T>* O2 = two ? a.sout[o + 1] + sline : nullptr;
+    for (int idx = lane; idx < nl * Kz1; idx += 32) {
+      const int k = idx / nl, l = idx - (idx / nl) * nl;
+      const Cx<T> Z = xbuf[l * L + k];
+      Cx<T> Zm = xbuf[l * L + (k == 0 ? 0 : L - k)];
+      Zm.y = -Zm.y;
+      O1[k * kzs + l] = cx<T>((T)0.5 * (Z.x + Zm.x), (T)0.5 * (Z.y + Zm.y));
+      if (two) O2[k * kzs + l] = cx<T>((T)0.5 * (Z.y - Zm.y), (T)-0.5 * (Z.x - Zm.x));
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// forward y pass: S [o][kz][x][y] -> I [o][kz][ky][x] (band ky kept)
+// ---------------------------------------------------------------------------
+template <typename T, class S>
+__global__ void __launch_bounds__(kWarps * 32) k_yfwd(const Cx<T>* __restrict__ in, Cx<T>* __restrict__ out,
+                                                       PadGeom g, const double2* __restrict__ twg) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Cx<T>* tw = (Cx<T>*)smem_raw;
+  Cx<T>* tile = tw + S::L + (threadIdx.x >> 5) * S::TILE;
+  constexpr int LPC = kWarps * S::LPW;
+  const int P0 = g.P[0], K1 = g.K[1], B1 = g.B[1];
+  const int nxb = (P0 + LPC - 1) / LPC;
+  const int per = g.Kz1 * nxb;
+  const int f = blockIdx.x / per;
+  const int r = blockIdx.x - f * per;
+  const int kz = r / nxb;
+  const int x0 = (r - kz * nxb) * LPC + (threadIdx.x >> 5) * S::LPW;
+  load_tw<T>(tw, twg, S::L);
+  __syncthreads();
+  const int nl = min(S::LPW, P0 - x0);
+  if (nl <= 0) return;
+  const Cx<T>* src = in + f * g.ns + ((int64_t)kz * P0 + x0) * S::L;
+  Cx<T>* dst = out + f * g.n1 + (int64_t)kz * B1 * P0 + x0;
+  auto load = [&](int line, int y) -> Cx<T> { return src[line * S::L + y]; };
+  auto store = [&](int line, int q, int, Cx<T> v) {
+    const int iy = bin_to_index(q, S::L, K1, B1);
+    if (iy >= 0) dst[iy * P0 + line] = v;
+  };
+  wfft<T, S, false>(tile, tw, nl, load, store);
+}
+
+// ---------------------------------------------------------------------------
+// forward x pass + epilogue: I [..][kz][ky][x] -> band, multipliers, 1/P^3,
+// -(v + .) / negation, fused RK4 stage update (kz = 0 deferred to k_fix0)
+// ---------------------------------------------------------------------------
+constexpr int kMaxFwd = 18;
+enum FwdMode { kEpiPlain = 0, kEpiNeg = 1, kEpiNegAdd = 2 };
+
+template <typename T>
+struct FwdOut {
+  int f[3];         // I-layout input fields
+  int axis[3];      // post-transform derivative 3-axis or -1
+  int nterms;
+  int mode;
+  const Cx<T>* vt;  // H-layout component for kEpiNegAdd
+};
+
+template <typename T>
+struct FwdArgs {
+  FwdOut<T> o[kMaxFwd];
+  int no;
+  const Cx<T>* in;  // I layout
+  T scale;
+  Cx<T>* z0;        // [no][B0*B1] raw kz = 0 plane
+  Cx<T>* kout;      // H layout [no][nh] or nullptr
+  int rk_s;         // 0: no RK4 update
+  T cs, h6;
+  Cx<T>* cur;
+  Cx<T>* acc;
+  Cx<T>* stage;
+};
+
+template <typename T>
+__device__ __forceinline__ void epilogue(const FwdArgs<T>& a, const FwdOut<T>& O, int64_t h, int64_t vidx, Cx<T> r) {
+  Cx<T> k;
+  if (O.mode == kEpiNegAdd) {
+    const Cx<T> v = O.vt[vidx];
+    k = cx<T>(-(v.x + r.x), -(v.y + r.y));
+  } else if (O.mode == kEpiNeg) {
+    k = cx<T>(-r.x, -r.y);
+  } else {
+    k = r;
+  }
+  if (a.kout) a.kout[h] = k;
+  if (a.rk_s) {
+    const Cx<T> cc = a.cur[h];
+    Cx<T> ac;
+    const int s = a.rk_s;
+    if (s == 1) {
+      ac = k;
+    } else {
+      ac = a.acc[h];
+      const T m = s < 4 ? (T)2 : (T)1;
+      ac = cx<T>(ac.x + m * k.x, ac.y + m * k.y);
+    }
+    if (s < 4) {
+      a.acc[h] = ac;
+      a.stage[h] = cx<T>(cc.x + a.cs * k.x, cc.y + a.cs * k.y);
+    } else {
+      a.cur[h] = cx<T>(cc.x + a.h6 * ac.x, cc.y + a.h6 * ac.y);
+    }
+  }
+}
+
+template <typename T, class S>
+__global__ void __launch_bounds__(kWarps * 32) k_xfwd(FwdArgs<T> a, PadGeom g, const double2* __restrict__ twg) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Cx<T>* tw = (Cx<T>*)smem_raw;
+  Cx<T>* tile = tw + S::L + (threadIdx.x >> 5) * S::TILE;
+  constexpr int LPC = kWarps * S::LPW;
+  const int K0 = g.K[0], B0 = g.B[0], B1 = g.B[1];
+  const int nyb = (B1 + LPC - 1) / LPC;
+  const int per = g.Kz1 * nyb;
+  const int o = blockIdx.x / per;
+  const int r = blockIdx.x - o * per;
+  const int kz = r / nyb;
+  const int ky0 = (r - kz * nyb) * LPC + (threadIdx.x >> 5) * S::LPW;
+  load_tw<T>(tw, twg, S::L);
+  __syncthreads();
+  const int nl = min(S::LPW, B1 - ky0);
+  if (nl <= 0) return;
+  const FwdOut<T>& O = a.o[o];
+  const T kzk = (T)(kTwoPi * (double)kz);
+  Cx<T> acc[S::R2];
+#pragma unroll
+  for (int i = 0; i < S::R2; ++i) acc[i] = cx<T>(0, 0);
+  const int lane = threadIdx.x & 31;
+  const int bline = lane / S::R1;
+  const int k1 = lane - bline * S::R1;
+  for (int t = 0; t < O.nterms; ++t) {
+    const Cx<T>* src = a.in + O.f[t] * g.n1 + ((int64_t)kz * B1 + ky0) * S::L;
+    const int ax = O.axis[t];
+    auto load = [&](int line, int x) -> Cx<T> { return src[line * S::L + x]; };
+    auto store = [&](int line, int q, int k2, Cx<T> v) {
+      const int ix = bin_to_index(q, S::L, K0, B0);
+      if (ix < 0) return;
+      if (ax == 0) v = mul_ik<T>(v, (T)(kTwoPi * (double)freq_of(ix, K0, B0)));
+      else if (ax == 1) v = mul_ik<T>(v, (T)(kTwoPi * (double)freq_of(ky0 + line, g.K[1], B1)));
+      else if (ax == 2) v = mul_ik<T>(v, kzk);
+      acc[k2] = cadd(acc[k2], v);
+    };
+    wfft<T, S, false>(tile, tw, nl, load, store);
+  }
+  if (bline >= nl || bline >= S::LPW) return;
+  const int ky = ky0 + bline;
+#pragma unroll
+  for (int k2 = 0; k2 < S::R2; ++k2) {
+    const int ix = bin_to_index(k1 + S::R1 * k2, S::L, K0, B0);
+    if (ix < 0) continue;
+    const Cx<T> rr = cscale(acc[k2], a.scale);
+    if (kz == 0) {
+      a.z0[(int64_t)o * B0 * B1 + ix * B1 + ky] = rr;
+    } else {
+      const int64_t e = ((int64_t)kz * B0 + ix) * B1 + ky;
+      epilogue<T>(a, O, (int64_t)o * g.nh + e, e, rr);
+    }
+  }
+}
+
+// kz = 0 plane: symmetrize pairs (k, -k), then the same epilogue
+template <typename T>
+__global__ void k_fix0(FwdArgs<T> a, PadGeom g) {
+  const int B0 = g.B[0], B1 = g.B[1];
+  const int64_t plane = (int64_t)B0 * B1;
+  const int64_t total = plane * a.no;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int o = (int)(i / plane);
+    const int e = (int)(i - o * plane);
+    const int ix = e / B1, iy = e - ix * B1;
+    const int mx = ix == 0 ? 0 : B0 - ix, my = iy == 0 ? 0 : B1 - iy;
+    const int e2 = mx * B1 + my;
+    const Cx<T> p = a.z0[o * plane + e], q = a.z0[o * plane + e2];
+    const Cx<T> r = cx<T>((T)0.5 * (p.x + q.x), (T)0.5 * (p.y - q.y));
+    epilogue<T>(a, a.o[o], (int64_t)o * g.nh + e, e, r);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// layout conversion: full block [comp][kx][ky][kz] <-> H layout [comp][kz][kx][ky]
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_full_to_h(const Cx<T>* __restrict__ full, int ncomp, PadGeom g, Cx<T>* __restrict__ H) {
+  const int64_t total = g.nh * ncomp;
+  const int B0 = g.B[0], B1 = g.B[1], B2 = g.B[2];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i / g.nh);
+    int64_t r = i - c * g.nh;
+    const int iy = (int)(r % B1);
+    r /= B1;
+    const int ix = (int)(r % B0);
+    const int kz = (int)(r / B0);
+    H[i] = full[(int64_t)c * B0 * B1 * B2 + ((int64_t)ix * B1 + iy) * B2 + kz];
+  }
+}
+
+template <typename T>
+__global__ void k_h_to_full(const Cx<T>* __restrict__ H, int ncomp, PadGeom g, Cx<T>* __restrict__ full) {
+  const int B0 = g.B[0], B1 = g.B[1], B2 = g.B[2];
+  const int64_t nb = (int64_t)B0 * B1 * B2;
+  const int64_t total = nb * ncomp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i / nb);
+    int64_t r = i - c * nb;
+    const int iz = (int)(r % B2);
+    r /= B2;
+    const int iy = (int)(r % B1);
+    const int ix = (int)(r / B1);
+    const Cx<T>* Hc = H + c * g.nh;
+    if (iz <= g.K[2]) {
+      full[i] = Hc[((int64_t)iz * B0 + ix) * B1 + iy];
+    } else {
+      const int kz = B2 - iz;
+      const int mx = ix == 0 ? 0 : B0 - ix, my = iy == 0 ? 0 : B1 - iy;
+      full[i] = cconj(Hc[((int64_t)kz * B0 + mx) * B1 + my]);
+    }
+  }
+}
+
+
+struct PadEngine {
+  bool ok = false;
+  bool tried = false;
+  PadGeom g{};
+  double2* tw[3] = {nullptr, nullptr, nullptr};
+  int line_smem_max = 0;
+};
+
+
+template <class K>
+static void ensure_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) BLR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+template <typename T, class S>
+void launch_xinv(blr_ctx* c, PadEngine* e, const XPassArgs<T>& a) {
+  const PadGeom& g = e->g;
+  constexpr int LPC = kWarps * S::LPW;
+  const size_t sm = sizeof(Cx<T>) * (S::L + kWarps * S::TILE);
+  ensure_smem(k_xinv<T, S>, sm);
+  const int nyb = (g.B[1] + LPC - 1) / LPC;
+  k_xinv<T, S><<<a.nx * g.Kz1 * nyb, kWarps * 32, sm, c->stream>>>(a, g, e->tw[0]);
+  BLR_LAUNCHED();
+}
+template <typename T, class S>
+void launch_yinv(blr_ctx* c, PadEngine* e, const YPassArgs<T>& a) {
+  const PadGeom& g = e->g;
+  constexpr int LPC = kWarps * S::LPW;
+  const size_t sm = sizeof(Cx<T>) * (S::L + kWarps * S::TILE);
+  ensure_smem(k_yinv<T, S>, sm);
+  const int nxb = (g.P[0] + LPC - 1) / LPC;
+  k_yinv<T, S><<<a.ny * g.Kz1 * nxb, kWarps * 32, sm, c->stream>>>(a, g, e->tw[1]);
+  BLR_LAUNCHED();
+}
+template <typename T, class S, int OP>
+void launch_lines(blr_ctx* c, PadEngine* e, const LineArgs<T>& a) {
+  const PadGeom& g = e->g;
+  const int ns_blk = OP == kOpContract ? a.d : a.ns;
+  const int nreal = (ZOp<OP>::acc || OP == kOpRealize) ? 0 : ns_blk;
+  const size_t warp_bytes = sizeof(Cx<T>) * ((size_t)S::TILE + 4 * (size_t)g.Kz1 * S::LPW + (size_t)S::LPW * S::L) +
+                            sizeof(T) * (size_t)nreal * S::LPW * S::L;
+  const size_t sm = S::L * sizeof(Cx<T>) + kZWarps * warp_bytes;
+  if (sm > (size_t)e->line_smem_max) throw Error(1, "z-line kernel shared memory exceeds the device limit");
+  static bool attr_done[2] = {false, false};
+  if (!attr_done[sizeof(T) == 8 ? 0 : 1]) {
+    BLR_CUDA(cudaFuncSetAttribute(k_zlines<T, S, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, e->line_smem_max));
+    attr_done[sizeof(T) == 8 ? 0 : 1] = true;
+  }
+  constexpr int LPC = kZWarps * S::LPW;
+  const int nyc = (g.P[1] + LPC - 1) / LPC;
+  k_zlines<T, S, OP><<<g.P[0] * nyc, kZWarps * 32, sm, c->stream>>>(a, g, e->tw[2]);
+  BLR_LAUNCHED();
+}
+template <typename T, class S>
+void launch_yfwd(blr_ctx* c, PadEngine* e, const Cx<T>* in, int nf, Cx<T>* out) {
+  const PadGeom& g = e->g;
+  constexpr int LPC = kWarps * S::LPW;
+  const size_t sm = sizeof(Cx<T>) * (S::L + kWarps * S::TILE);
+  ensure_smem(k_yfwd<T, S>, sm);
+  const int nxb = (g.P[0] + LPC - 1) / LPC;
+  k_yfwd<T, S><<<nf * g.Kz1 * nxb, kWarps * 32, sm, c->stream>>>(in, out, g, e->tw[1]);
+  BLR_LAUNCHED();
+}
+template <typename T, class S>
+void launch_xfwd(blr_ctx* c, PadEngine* e, const FwdArgs<T>& a) {
+  const PadGeom& g = e->g;
+  constexpr int LPC = kWarps * S::LPW;
+  const size_t sm = sizeof(Cx<T>) * (S::L + kWarps * S::TILE);
+  ensure_smem(k_xfwd<T, S>, sm);
+  const int nyb = (g.B[1] + LPC - 1) / LPC;
+  k_xfwd<T, S><<<a.no * g.Kz1 * nyb, kWarps * 32, sm, c->stream>>>(a, g, e->tw[0]);
+  BLR_LAUNCHED();
+}
+
+
+}  // namespace blr

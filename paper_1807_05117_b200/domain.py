@@ -7,7 +7,7 @@
   reference uses ``next_fast_len(4K+1)`` (``spectral.py:239-242``); any
   ``P >= 3K+1`` gives the exact truncated convolution because every pad-grid
   product is bilinear in K-band fields, so the default is the smallest
-  7-smooth size >= 3K+1 (e.g. 98 instead of 132 at K=32, 2.4x fewer points).
+  engine length >= 3K+1 (e.g. 100 instead of 132 at K=32, 2.3x fewer points).
 * ``dtype`` — ``"float64"`` (parity mode, complex128 blocks) or ``"float32"``.
 * ``device`` — CUDA device index.
 """
@@ -40,8 +40,20 @@ def smooth_size(n: int, primes=(2, 3, 5, 7)) -> int:
         m += 1
 
 
+# Pad lengths the fused sm_100a pad engine implements (L = R1*R2 warp FFTs,
+# csrc/blr_fft.cuh BLR_FOR_EACH_L); other 7-smooth pads run the cuFFT path.
+ENGINE_PADS = (10, 14, 16, 20, 25, 28, 32, 40, 49, 50, 64, 100, 196)
+
+
 def default_pad(bandwidth) -> tuple:
-    return tuple(smooth_size(3 * k + 1) for k in bandwidth)
+    """Smallest engine pad >= 3K+1 per axis (exact truncated convolution),
+    else the smallest 7-smooth size >= 3K+1."""
+    out = []
+    for k in bandwidth:
+        need = 3 * k + 1
+        fast = [p for p in ENGINE_PADS if p >= need]
+        out.append(fast[0] if fast else smooth_size(need))
+    return tuple(out)
 
 
 @dataclass(frozen=True)
