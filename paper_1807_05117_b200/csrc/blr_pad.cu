@@ -210,12 +210,16 @@ template <typename T>
 static void acc_tables(int op, LineArgs<T>& a) {
   const int d = a.d, dd = d * d;
   for (int f = 0; f < kMaxLineS; ++f) { a.oi[f] = 0; a.ri[f] = 0; a.sg[f] = 1.0; }
+  a.nst = 0;
   if (op == kOpMap || op == kOpMapTC) {
-    for (int f = 0; f < dd; ++f) {
-      a.oi[f] = f / d;
-      a.ri[f] = (op == kOpMap ? 0 : dd) + f % d;
-    }
+    // staged slots: V_j
+    a.nst = d;
+    for (int j = 0; j < d; ++j) a.st_idx[j] = (op == kOpMap ? 0 : dd) + j;
+    for (int f = 0; f < dd; ++f) { a.oi[f] = f / d; a.ri[f] = f % d; }
   } else if (op == kOpInvVol) {
+    // staged slots: V_0..V_{d-1}, Dv
+    a.nst = d + 1;
+    for (int j = 0; j <= d; ++j) a.st_idx[j] = j;
     for (int f = 0; f < dd; ++f) { a.oi[f] = f / d; a.ri[f] = f % d; }
     for (int q = 0; q < d; ++q) { a.oi[dd + q] = d; a.ri[dd + q] = q; a.sg[dd + q] = -1.0; }
     a.oi[dd + d] = d; a.ri[dd + d] = d; a.sg[dd + d] = -1.0;

@@ -94,10 +94,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_xinv(XPassArgs<T> a, PadGeom g,
   Cx<T>* out = a.out + xf * g.n1 + ((int64_t)kz * B1 + ky0) * S::L;
   auto load = [&](int line, int p) -> Cx<T> {
     const int ix = bin_to_index(p, S::L, K0, B0);
-    if (ix < 0) return cx<T>(0, 0);
-    Cx<T> z = src[ix * B1 + line];
-    if (mulx) z = mul_ik<T>(z, (T)(kTwoPi * (double)freq_of(ix, K0, B0)));
-    return z;
+    const bool ok = ix >= 0;
+    const int ixc = ok ? ix : 0;
+    Cx<T> z = src[ixc * B1 + line];
+    if (mulx) z = mul_ik<T>(z, (T)(kTwoPi * (double)freq_of(ixc, K0, B0)));
+    return ok ? z : cx<T>(0, 0);
   };
   auto store = [&](int line, int x, int, Cx<T> v) { out[line * S::L + x] = v; };
   wfft<T, S, true>(tile, tw, nl, load, store);
@@ -137,22 +138,26 @@ __global__ void __launch_bounds__(kWarps * 32) k_yinv(YPassArgs<T> a, PadGeom g,
   const Cx<T>* src[3];
   int ax[3];
   for (int t = 0; t < 3; ++t) {
-    src[t] = t < nt ? a.in + a.xf[yf][t] * g.n1 + (int64_t)kz * B1 * P0 + x0 : nullptr;
-    ax[t] = a.axis[yf][t];
+    // absent terms read term 0 (always valid) and are masked out
+    src[t] = a.in + a.xf[yf][t < nt ? t : 0] * g.n1 + (int64_t)kz * B1 * P0 + x0;
+    ax[t] = t < nt ? a.axis[yf][t] : -2;
   }
   const T kzk = (T)(kTwoPi * (double)kz);
   Cx<T>* out = a.out + yf * g.ns + ((int64_t)kz * P0 + x0) * S::L;
   auto load = [&](int line, int q) -> Cx<T> {
     const int iy = bin_to_index(q, S::L, K1, B1);
+    const bool ok = iy >= 0;
+    const int iyc = ok ? iy : 0;
+    const T ky = (T)(kTwoPi * (double)freq_of(iyc, K1, B1));
     Cx<T> acc = cx<T>(0, 0);
-    if (iy < 0) return acc;
-    for (int t = 0; t < nt; ++t) {
-      Cx<T> z = src[t][iy * P0 + line];
-      if (ax[t] == 1) z = mul_ik<T>(z, (T)(kTwoPi * (double)freq_of(iy, K1, B1)));
-      else if (ax[t] == 2) z = mul_ik<T>(z, kzk);
-      acc = cadd(acc, z);
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      Cx<T> z = src[t][iyc * P0 + line];
+      const T m = ax[t] == 1 ? ky : kzk;
+      if (ax[t] >= 1) z = mul_ik<T>(z, m);
+      if (ax[t] >= -1) acc = cadd(acc, z);
     }
-    return acc;
+    return ok ? acc : cx<T>(0, 0);
   };
   auto store = [&](int line, int y, int, Cx<T> v) { out[line * S::L + y] = v; };
   wfft<T, S, true>(tile, tw, nl, load, store);
@@ -193,8 +198,10 @@ struct LineArgs {
   double w[32];
   int transpose;
   // ACC-op tables (host-built): output index, real-input index and sign per field
-  int oi[kMaxLineS], ri[kMaxLineS];
+  int oi[kMaxLineS], ri[kMaxLineS];  // ri: staged-slot index for ACC ops
   double sg[kMaxLineS];
+  int nst;                           // real fields staged in shared memory (ACC ops)
+  int st_idx[4];                     // their rin indices
   int mi[3][3];  // contraction: rin index of M(o, j)
 };
 
@@ -281,16 +288,19 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
   const int y0 = (blockIdx.x - x * nyc) * LPC + warp * S::LPW;
   const int ns_blk = OP == kOpContract ? a.d : a.ns;
   const int nreal = (Tr::acc || OP == kOpRealize) ? 0 : ns_blk;
-  // shared layout: tw | per warp { tile | stage[2][2][Kz1*LPW] | xbuf[LPW*L] | Rsm[nreal][LPW*L] }
-  const int stage_n = 2 * 2 * Kz1 * S::LPW;
-  const size_t warp_bytes =
-      sizeof(Cx<T>) * ((size_t)S::TILE + stage_n + (size_t)S::LPW * L) + sizeof(T) * (size_t)nreal * S::LPW * L;
+  // shared layout: tw | per warp { tile | stage[max(2*2*Kz1*LPW, LPW*L)] (xbuf aliases it after the
+  //                                 C2R phase) | Vst[nst][LPW*L] | Rsm[nreal][LPW*L] }
+  const int stage_n = max(2 * 2 * Kz1 * S::LPW, S::LPW * L);
+  const int nst = Tr::acc ? a.nst : 0;
+  const size_t warp_bytes = sizeof(Cx<T>) * ((size_t)S::TILE + stage_n) +
+                            sizeof(T) * (size_t)(nreal + nst) * S::LPW * L;
   Cx<T>* tw = (Cx<T>*)smem_raw;
   unsigned char* wb = smem_raw + sizeof(Cx<T>) * L + warp * warp_bytes;
   Cx<T>* tile = (Cx<T>*)wb;
   Cx<T>* stage = tile + S::TILE;
-  Cx<T>* xbuf = stage + stage_n;
-  T* Rsm = (T*)(xbuf + S::LPW * L);
+  Cx<T>* xbuf = stage;
+  T* Vst = (T*)(stage + stage_n);
+  T* Rsm = Vst + nst * S::LPW * L;
   const int ldR = S::LPW * L;
   load_tw<T>(tw, twz_g, L);
   __syncthreads();
@@ -299,6 +309,19 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
   const int64_t sline = (int64_t)x * P1 + y0;
   const int64_t kzs = (int64_t)P0 * P1;
   const int64_t rline = ((int64_t)x * P1 + y0) * L;
+  // stage the real fields the contributions read (contiguous nl*L run per field)
+  for (int q = 0; q < nst; ++q) {
+    const T* src = a.rin[a.st_idx[q]] + rline;
+    T* dst = Vst + q * ldR;
+    constexpr int V = 16 / sizeof(T);  // elements per 16-byte copy
+    if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+      const int nv = (nl * L) / V;
+      for (int i = lane; i < nv; i += 32) __pipeline_memcpy_async(dst + V * i, src + V * i, 16);
+      for (int i = nv * V + lane; i < nl * L; i += 32) __pipeline_memcpy_async(dst + i, src + i, sizeof(T));
+    } else {
+      for (int i = lane; i < nl * L; i += 32) __pipeline_memcpy_async(dst + i, src + i, sizeof(T));
+    }
+  }
   // step-B ownership: lane (bl, k1) owns z = k1 + R1*k2
   const int bl = lane / S::R1, k1 = lane - (lane / S::R1) * S::R1;
   const bool own = bl < nl && bl < S::LPW;
@@ -308,19 +331,32 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
 #pragma unroll
     for (int k2 = 0; k2 < S::R2; ++k2) acc[o][k2] = 0;
   if constexpr (OP == kOpMapTC) {
-    // acc_i = sum_j Du_ij dV_j  (rin: Du [0,dd) V [dd,dd+d) dV [dd+d, dd+2d))
+    // acc_i = sum_j Du_ij dV_j  (rin: Du [0,dd) V [dd,dd+d) dV [dd+d, dd+2d)); branch-free
+    // unrolled loads (absent components read component 0 and are masked)
     if (own) {
       const int d = a.d, dd = d * d;
+      const T* du[3][3];
+      const T* dv[3];
+      T msk[3];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int jc = j < d ? j : 0;
+        msk[j] = j < d ? (T)1 : (T)0;
+        dv[j] = a.rin[dd + d + jc] + rline + bl * L + k1;
+#pragma unroll
+        for (int o = 0; o < 3; ++o) du[o][j] = a.rin[(o < d ? o : 0) * d + jc] + rline + bl * L + k1;
+      }
 #pragma unroll
       for (int k2 = 0; k2 < S::R2; ++k2) {
-        const int64_t gi = rline + bl * L + k1 + S::R1 * k2;
+        T vj[3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) vj[j] = msk[j] * __ldg(dv[j] + S::R1 * k2);
 #pragma unroll
         for (int o = 0; o < NOM; ++o) {
-          if (o < d) {
-            T s = 0;
-            for (int j = 0; j < d; ++j) s += __ldg(a.rin[o * d + j] + gi) * __ldg(a.rin[dd + d + j] + gi);
-            acc[o][k2] = s;
-          }
+          T s = 0;
+#pragma unroll
+          for (int j = 0; j < 3; ++j) s += __ldg(du[o < 3 ? o : 0][j] + S::R1 * k2) * vj[j];
+          acc[o][k2] = s;
         }
       }
     }
@@ -400,8 +436,8 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
           if (two) a.wout[f + 1][gi] = v.y;
         }
         const int o1 = a.oi[f], o2 = two ? a.oi[f + 1] : -1;
-        const T c1 = a.sg[f] * v.x * __ldg(a.rin[a.ri[f]] + gi);
-        const T c2 = two ? a.sg[f + 1] * v.y * __ldg(a.rin[a.ri[f + 1]] + gi) : (T)0;
+        const T c1 = (T)a.sg[f] * v.x * Vst[a.ri[f] * ldR + li];
+        const T c2 = two ? (T)a.sg[f + 1] * v.y * Vst[a.ri[f + 1] * ldR + li] : (T)0;
 #pragma unroll
         for (int o = 0; o < NOM; ++o) {
           if (o == o1) acc[o][k2] += c1;
@@ -706,8 +742,10 @@ void launch_lines(blr_ctx* c, PadEngine* e, const LineArgs<T>& a) {
   const PadGeom& g = e->g;
   const int ns_blk = OP == kOpContract ? a.d : a.ns;
   const int nreal = (ZOp<OP>::acc || OP == kOpRealize) ? 0 : ns_blk;
-  const size_t warp_bytes = sizeof(Cx<T>) * ((size_t)S::TILE + 4 * (size_t)g.Kz1 * S::LPW + (size_t)S::LPW * S::L) +
-                            sizeof(T) * (size_t)nreal * S::LPW * S::L;
+  const int nst = ZOp<OP>::acc ? a.nst : 0;
+  const size_t stage_n = std::max<size_t>(4 * (size_t)g.Kz1 * S::LPW, (size_t)S::LPW * S::L);
+  const size_t warp_bytes = sizeof(Cx<T>) * ((size_t)S::TILE + stage_n) +
+                            sizeof(T) * (size_t)(nreal + nst) * S::LPW * S::L;
   const size_t sm = S::L * sizeof(Cx<T>) + kZWarps * warp_bytes;
   if (sm > (size_t)e->line_smem_max) throw Error(1, "z-line kernel shared memory exceeds the device limit");
   static bool attr_done[2] = {false, false};
