@@ -54,6 +54,10 @@ def fourier_warp(domain: Domain, values, displacement) -> torch.Tensor:
     """Trigonometric interpolant at ``x + u(x)`` (gridops.py:51-75), verification only."""
     shape, d = domain.shape, domain.ndim
     f = as_grid(domain, values).double()
+    if f.dim() > d:  # stack of images sharing one displacement
+        flat = f.reshape((-1,) + shape)
+        return torch.stack([fourier_warp(domain, x, displacement) for x in flat]).reshape(f.shape).to(
+            domain.rdtype)
     u = as_grid(domain, displacement).double()
     spec = torch.fft.fftn(f) / float(np.prod(shape))
     npts = int(np.prod(shape))

@@ -1,0 +1,90 @@
+"""End-to-end parity of the B200 path against the unmodified reference.
+
+* Config 1 (2-D 64^2, K=16, alpha 0.01, sigma2 0.03, GN, 30 outer;
+  tests/test_solver.py:122-127 in the reference) for both objectives: the
+  discrete trace (PCG iterations, accepted steps, negative-curvature flags,
+  status) must be identical; final energy / MSE_rel / Jacobian extrema within
+  the SURVEY §8(d) tolerances (deformation: 1e-9 / 1e-8 / 1e-8; state, whose
+  stall regime amplifies rounding: 1e-4 / 1e-4 / 1e-3).
+* 3-D 64^3 / K=16 checksums (energy 1e-12, GN HVP norm 1e-10).
+* 3-D 128^3 / K=32 golden scalars recorded in SURVEY.md §8(c).
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from golden_io import exists, load  # noqa: E402
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import blreg_oracle as O  # noqa: E402
+import paper_1807_05117_b200 as B  # noqa: E402
+from paper_1807_05117_b200 import gridops, spectral  # noqa: E402
+
+
+@pytest.mark.skipif(not exists("solver_config1"), reason="fixture needs make_golden --slow")
+@pytest.mark.parametrize("kind", ["def", "state"])
+def test_config1_registration_trace(kind):
+    g = load("solver_config1")
+    dom = B.Domain((64, 64), (16, 16), alpha=0.01, order=2)
+    cls = B.DeformationObjective if kind == "def" else B.StateObjective
+    obj = cls(dom, g["source"], g["target"], B.ProblemConfig(sigma2=0.03))
+    cfg = B.SolverConfig(method="gauss_newton", max_outer=30, grad_tol=0.01)
+    res = B.minimize(obj, B.TimeFlow.zero(dom), cfg)
+    assert res.status == str(g[f"{kind}_status"])
+    assert [r.pcg_iters for r in res.records] == list(g[f"{kind}_pcg"])
+    assert [r.negative_curvature for r in res.records] == list(g[f"{kind}_negc"])
+    assert [r.step for r in res.records] == pytest.approx(list(g[f"{kind}_step"]), rel=0, abs=0)
+    assert res.total_pcg_iters == int(g[f"{kind}_total_pcg"])
+    jd = gridops.jacobian_determinant(dom, spectral.include(dom, res.evaluation.cache.forward[-1],
+                                                             check=False))
+    e_tol, m_tol, j_tol = (1e-9, 1e-8, 1e-8) if kind == "def" else (1e-4, 1e-4, 1e-3)
+    assert res.evaluation.energy == pytest.approx(float(g[f"{kind}_final_energy"]), rel=e_tol)
+    assert res.final_mse_rel == pytest.approx(float(g[f"{kind}_final_mse"]), rel=m_tol)
+    assert float(jd.min()) == pytest.approx(float(g[f"{kind}_jmin"]), rel=j_tol)
+    assert float(jd.max()) == pytest.approx(float(g[f"{kind}_jmax"]), rel=j_tol)
+    np.testing.assert_allclose([r.energy for r in res.records], g[f"{kind}_energy"],
+                               rtol=e_tol * 10)
+
+
+@pytest.mark.skipif(not exists("checksum_64"), reason="fixture needs make_golden --slow")
+@pytest.mark.parametrize("kind", ["state", "def"])
+def test_checksum_64(kind):
+    g = load("checksum_64")
+    odom = O.Dom((64,) * 3, (16,) * 3, alpha=0.02, order=2)
+    rng = np.random.default_rng(0)
+    I0, I1 = O.band_image(odom, rng), O.band_image(odom, rng)
+    v = O.smooth_vector_block(odom, rng, 0.5 / 64, decay=2.0)[None]
+    w = O.smooth_vector_block(odom, rng, 0.5 / 64, decay=2.0)[None]
+    dom = B.Domain((64,) * 3, (16,) * 3, alpha=0.02, order=2)
+    cls = B.StateObjective if kind == "state" else B.DeformationObjective
+    obj = cls(dom, I0, I1, B.ProblemConfig(sigma2=0.1))
+    ev = obj.gradient(B.TimeFlow(dom, v, 10, True))
+    assert ev.energy == pytest.approx(float(g[f"{kind}_energy"]), rel=1e-12)
+    hw = ev.hessian_vector(B.TimeFlow(dom, w, 10, True), gauss_newton=True).values
+    assert float(torch.linalg.norm(hw)) == pytest.approx(float(g[f"{kind}_hvp_norm"]), rel=1e-10)
+    assert spectral.inner(hw, spectral.as_band(dom, w), dom) == pytest.approx(
+        float(g[f"{kind}_hvp_dot_w"]), rel=1e-10)
+    assert float(torch.linalg.norm(ev.gradient.values)) == pytest.approx(
+        float(g[f"{kind}_grad_norm"]), rel=1e-10)
+
+
+@pytest.mark.parametrize("kind,hnorm", [("state", 5.304078e-01), ("def", 5.304107e-01)])
+def test_survey_scalars_128(kind, hnorm):
+    """reference E and |Hw| at 128^3/K=32 (recorded in the survey)."""
+    odom = O.Dom((128,) * 3, (32,) * 3, alpha=0.02, order=2)
+    rng = np.random.default_rng(0)
+    I0, I1 = O.band_image(odom, rng), O.band_image(odom, rng)
+    v = O.smooth_vector_block(odom, rng, 0.5 / 128, decay=2.0)[None]
+    w = O.smooth_vector_block(odom, rng, 0.5 / 128, decay=2.0)[None]
+    dom = B.Domain((128,) * 3, (32,) * 3, alpha=0.02, order=2)
+    cls = B.StateObjective if kind == "state" else B.DeformationObjective
+    obj = cls(dom, I0, I1, B.ProblemConfig(sigma2=0.1))
+    ev = obj.gradient(B.TimeFlow(dom, v, 10, True))
+    assert ev.energy == pytest.approx(0.7762438153874031, rel=1e-12)
+    hw = ev.hessian_vector(B.TimeFlow(dom, w, 10, True), gauss_newton=True).values
+    assert float(torch.linalg.norm(hw)) == pytest.approx(hnorm, rel=2e-6)
