@@ -203,6 +203,25 @@ def checksum_case(name, n, k):
     save(name, **dom_meta(dom), **out)
 
 
+def volio_case(name):
+    """BLVOL files written by the reference writer (volio.py), stored as bytes."""
+    import tempfile
+
+    from blreg import volio
+
+    rng = np.random.default_rng(21)
+    scalar = rng.standard_normal((5, 6, 7))
+    vector = rng.standard_normal((2, 9, 4))
+    out = dict(scalar=scalar, vector=vector)
+    with tempfile.TemporaryDirectory() as tmp:
+        for tag, arr, spacing in (("scalar", scalar, None), ("vector", vector, (0.5, 0.25))):
+            path = os.path.join(tmp, f"{tag}.vol")
+            volio.write_volume(path, arr, spacing)
+            with open(path, "rb") as fh:
+                out[f"{tag}_bytes"] = np.frombuffer(fh.read(), dtype=np.uint8)
+    save(name, **out)
+
+
 def main():
     slow = "--slow" in sys.argv
     spectral_case("spectral_3d", Domain((12, 16, 18), (3, 4, 5), alpha=0.05), 1)
@@ -230,6 +249,7 @@ def main():
                    ProblemConfig(sigma2=0.1, n_time_steps=6), stationary=False)
     objective_case("obj_2d_refine", Domain((32, 32), (8, 8), alpha=0.05), 17,
                    ProblemConfig(sigma2=0.1, n_time_steps=4), amp=0.3)
+    volio_case("volio")
     if slow:
         solver_case("solver_config1")
         checksum_case("checksum_64", 64, 16)
