@@ -362,7 +362,7 @@ struct WShape {
   static constexpr int TILE = LPW * TS;             // shared tile entries per warp
 };
 
-// step A: lanes (line, n2) gather x[R2*n1 + n2] with load(line, n), DFT_R1,
+// step A: lanes (line, n2) gather x[R2*n1 + n2] with load(line, n, n1), DFT_R1,
 // twiddle W_L^(n2 k1) (table tw[m] = exp(-2 pi i m / L)), store to the tile.
 template <typename T, class S, bool INV, class Load>
 __device__ __forceinline__ void wfft_a(Cx<T>* tile, const Cx<T>* tw, int nl, Load& load) {
@@ -371,7 +371,7 @@ __device__ __forceinline__ void wfft_a(Cx<T>* tile, const Cx<T>* tw, int nl, Loa
   if (line < nl && line < S::LPW) {
     Cx<T> v[S::R1];
 #pragma unroll
-    for (int n1 = 0; n1 < S::R1; ++n1) v[n1] = load(line, S::R2 * n1 + n2);
+    for (int n1 = 0; n1 < S::R1; ++n1) v[n1] = load(line, S::R2 * n1 + n2, n1);
     dft<T, S::R1, INV>(v);
     Cx<T>* t = tile + line * S::TS + n2;
 #pragma unroll

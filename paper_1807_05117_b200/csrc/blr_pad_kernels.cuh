@@ -43,6 +43,7 @@ struct PadGeom {
 };
 
 constexpr int kWarps = 8;  // warps per CTA in the x / y pass kernels
+constexpr int kPassMinBlocks = 1;  // occupancy hint for the pass kernels (4 tried: no gain, spills)
 
 __device__ __forceinline__ int bin_to_index(int p, int P, int K, int B) {
   if (p <= K) return p;
@@ -72,31 +73,50 @@ struct XPassArgs {
   Cx<T>* out;
 };
 
+template <typename T>
+__device__ __forceinline__ void cp_async(Cx<T>* dst, const Cx<T>* src) {
+  __pipeline_memcpy_async(dst, src, sizeof(Cx<T>));
+}
+
+// Staged pass kernels: kPW warps per CTA; the CTA's whole input slab is
+// copied to shared memory with coalesced cp.async first, then every warp runs
+// its four-step FFTs from shared memory.
+constexpr int kPW = 4;
+
 template <typename T, class S>
-__global__ void __launch_bounds__(kWarps * 32) k_xinv(XPassArgs<T> a, PadGeom g, const double2* __restrict__ twg) {
+__global__ void __launch_bounds__(kPW * 32) k_xinv(XPassArgs<T> a, PadGeom g, const double2* __restrict__ twg) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int LPC = kPW * S::LPW;
+  const int K0 = g.K[0], B0 = g.B[0], B1 = g.B[1];
   Cx<T>* tw = (Cx<T>*)smem_raw;
-  Cx<T>* tile = tw + S::L + (threadIdx.x >> 5) * S::TILE;
-  constexpr int LPC = kWarps * S::LPW;
-  const int nyb = (g.B[1] + LPC - 1) / LPC;
+  Cx<T>* slab = tw + S::L;                       // [B0][LPC]
+  Cx<T>* tile = slab + B0 * LPC + (threadIdx.x >> 5) * S::TILE;
+  const int nyb = (B1 + LPC - 1) / LPC;
   const int per = g.Kz1 * nyb;
   const int xf = blockIdx.x / per;
   const int r = blockIdx.x - xf * per;
   const int kz = r / nyb;
-  const int ky0 = (r - kz * nyb) * LPC + (threadIdx.x >> 5) * S::LPW;
+  const int cky0 = (r - kz * nyb) * LPC;
+  const int nlc = min(LPC, B1 - cky0);
+  const Cx<T>* src = a.src[xf] + ((int64_t)kz * B0) * B1 + cky0;
+  for (int i = threadIdx.x; i < B0 * LPC; i += blockDim.x) {
+    const int ix = i / LPC, l = i - ix * LPC;
+    if (l < nlc) cp_async<T>(slab + i, src + ix * B1 + l);
+  }
+  __pipeline_commit();
   load_tw<T>(tw, twg, S::L);
+  __pipeline_wait_prior(0);
   __syncthreads();
-  const int nl = min(S::LPW, g.B[1] - ky0);
+  const int wl0 = (threadIdx.x >> 5) * S::LPW;
+  const int nl = min(S::LPW, nlc - wl0);
   if (nl <= 0) return;
-  const int K0 = g.K[0], B0 = g.B[0], B1 = g.B[1];
-  const Cx<T>* src = a.src[xf] + ((int64_t)kz * B0) * B1 + ky0;
   const bool mulx = a.mulx[xf] != 0;
-  Cx<T>* out = a.out + xf * g.n1 + ((int64_t)kz * B1 + ky0) * S::L;
-  auto load = [&](int line, int p) -> Cx<T> {
+  Cx<T>* out = a.out + xf * g.n1 + ((int64_t)kz * B1 + cky0 + wl0) * S::L;
+  auto load = [&](int line, int p, int) -> Cx<T> {
     const int ix = bin_to_index(p, S::L, K0, B0);
     const bool ok = ix >= 0;
     const int ixc = ok ? ix : 0;
-    Cx<T> z = src[ixc * B1 + line];
+    Cx<T> z = slab[ixc * LPC + wl0 + line];
     if (mulx) z = mul_ik<T>(z, (T)(kTwoPi * (double)freq_of(ixc, K0, B0)));
     return ok ? z : cx<T>(0, 0);
   };
@@ -118,33 +138,41 @@ struct YPassArgs {
 };
 
 template <typename T, class S>
-__global__ void __launch_bounds__(kWarps * 32) k_yinv(YPassArgs<T> a, PadGeom g, const double2* __restrict__ twg) {
+__global__ void __launch_bounds__(kPW * 32) k_yinv(YPassArgs<T> a, PadGeom g, const double2* __restrict__ twg, int ntmax) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Cx<T>* tw = (Cx<T>*)smem_raw;
-  Cx<T>* tile = tw + S::L + (threadIdx.x >> 5) * S::TILE;
-  constexpr int LPC = kWarps * S::LPW;
+  constexpr int LPC = kPW * S::LPW;
   const int P0 = g.P[0], K1 = g.K[1], B1 = g.B[1];
+  Cx<T>* tw = (Cx<T>*)smem_raw;
+  Cx<T>* slab = tw + S::L;                       // [ntmax][B1][LPC]
+  Cx<T>* tile = slab + ntmax * B1 * LPC + (threadIdx.x >> 5) * S::TILE;
   const int nxb = (P0 + LPC - 1) / LPC;
   const int per = g.Kz1 * nxb;
   const int yf = blockIdx.x / per;
   const int r = blockIdx.x - yf * per;
   const int kz = r / nxb;
-  const int x0 = (r - kz * nxb) * LPC + (threadIdx.x >> 5) * S::LPW;
-  load_tw<T>(tw, twg, S::L);
-  __syncthreads();
-  const int nl = min(S::LPW, P0 - x0);
-  if (nl <= 0) return;
+  const int cx0 = (r - kz * nxb) * LPC;
+  const int nlc = min(LPC, P0 - cx0);
   const int nt = a.nterms[yf];
-  const Cx<T>* src[3];
-  int ax[3];
-  for (int t = 0; t < 3; ++t) {
-    // absent terms read term 0 (always valid) and are masked out
-    src[t] = a.in + a.xf[yf][t < nt ? t : 0] * g.n1 + (int64_t)kz * B1 * P0 + x0;
-    ax[t] = t < nt ? a.axis[yf][t] : -2;
+  for (int t = 0; t < nt; ++t) {
+    const Cx<T>* src = a.in + a.xf[yf][t] * g.n1 + (int64_t)kz * B1 * P0 + cx0;
+    Cx<T>* dst = slab + t * B1 * LPC;
+    for (int i = threadIdx.x; i < B1 * LPC; i += blockDim.x) {
+      const int iy = i / LPC, l = i - iy * LPC;
+      if (l < nlc) cp_async<T>(dst + i, src + iy * P0 + l);
+    }
   }
+  __pipeline_commit();
+  load_tw<T>(tw, twg, S::L);
+  __pipeline_wait_prior(0);
+  __syncthreads();
+  const int wl0 = (threadIdx.x >> 5) * S::LPW;
+  const int nl = min(S::LPW, nlc - wl0);
+  if (nl <= 0) return;
+  int ax[3];
+  for (int t = 0; t < 3; ++t) ax[t] = t < nt ? a.axis[yf][t] : -2;
   const T kzk = (T)(kTwoPi * (double)kz);
-  Cx<T>* out = a.out + yf * g.ns + ((int64_t)kz * P0 + x0) * S::L;
-  auto load = [&](int line, int q) -> Cx<T> {
+  Cx<T>* out = a.out + yf * g.ns + ((int64_t)kz * P0 + cx0 + wl0) * S::L;
+  auto load = [&](int line, int q, int) -> Cx<T> {
     const int iy = bin_to_index(q, S::L, K1, B1);
     const bool ok = iy >= 0;
     const int iyc = ok ? iy : 0;
@@ -152,10 +180,10 @@ __global__ void __launch_bounds__(kWarps * 32) k_yinv(YPassArgs<T> a, PadGeom g,
     Cx<T> acc = cx<T>(0, 0);
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
-      Cx<T> z = src[t][iyc * P0 + line];
-      const T m = ax[t] == 1 ? ky : kzk;
-      if (ax[t] >= 1) z = mul_ik<T>(z, m);
-      if (ax[t] >= -1) acc = cadd(acc, z);
+      if (ax[t] < -1) break;
+      Cx<T> z = slab[(t * B1 + iyc) * LPC + wl0 + line];
+      if (ax[t] >= 1) z = mul_ik<T>(z, ax[t] == 1 ? ky : kzk);
+      acc = cadd(acc, z);
     }
     return ok ? acc : cx<T>(0, 0);
   };
@@ -290,7 +318,8 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
   const int nreal = (Tr::acc || OP == kOpRealize) ? 0 : ns_blk;
   // shared layout: tw | per warp { tile | stage[max(2*2*Kz1*LPW, LPW*L)] (xbuf aliases it after the
   //                                 C2R phase) | Vst[nst][LPW*L] | Rsm[nreal][LPW*L] }
-  const int stage_n = max(2 * 2 * Kz1 * S::LPW, S::LPW * L);
+  const int fstride = (Kz1 + 1) * S::LPW;  // per-field stage: Kz1 spectra rows + one zero row
+  const int stage_n = max(2 * 2 * fstride, S::LPW * L);
   const int nst = Tr::acc ? a.nst : 0;
   const size_t warp_bytes = sizeof(Cx<T>) * ((size_t)S::TILE + stage_n) +
                             sizeof(T) * (size_t)(nreal + nst) * S::LPW * L;
@@ -361,6 +390,27 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
       }
     }
   }
+  // per-lane Hermitian gather table for step A (lane n2, rows k = R2*n1 + n2):
+  // stage row index and sign s: G = (F1.x - s F2.y, s F1.y + F2.x)
+  int hidx[S::R1], hsg[S::R1];
+  {
+    const int n2 = lane - (lane / S::R2) * S::R2;
+#pragma unroll
+    for (int n1 = 0; n1 < S::R1; ++n1) {
+      const int k = S::R2 * n1 + n2;
+      int row = Kz1, sgn = 1;  // zero row
+      if (k == 0) { row = 0; sgn = 0; }
+      else if (k <= K2) { row = k; sgn = 1; }
+      else if (k >= L - K2) { row = L - k; sgn = -1; }
+      hidx[n1] = row * S::LPW;
+      hsg[n1] = sgn;
+    }
+  }
+  // zero rows of both stage buffers (never overwritten by the prefetch)
+  for (int i = lane; i < 4 * S::LPW; i += 32) {
+    const int b = i / (2 * S::LPW), q = i - b * 2 * S::LPW;
+    stage[b * 2 * fstride + (q / S::LPW) * fstride + Kz1 * S::LPW + (q % S::LPW)] = cx<T>(0, 0);
+  }
   const int npair = (ns_blk + 1) / 2;
   const int nloop = OP == kOpContract ? a.n_nodes : 1;
   const int total = nloop * npair;
@@ -368,18 +418,22 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
   auto prefetch = [&](int q) {
     const int node = q / npair, p = q - node * npair;
     const int64_t noff = OP == kOpContract ? node * a.sin_node_stride : 0;
-    Cx<T>* st = stage + (q & 1) * 2 * Kz1 * S::LPW;
+    Cx<T>* st = stage + (q & 1) * 2 * fstride;
     for (int ff = 0; ff < 2; ++ff) {
       const int f = 2 * p + ff;
-      if (f >= ns_blk) break;
+      if (f >= ns_blk) {  // odd field count: the partner reads zeros
+        for (int i = lane; i < Kz1 * S::LPW; i += 32) st[ff * fstride + i] = cx<T>(0, 0);
+        break;
+      }
       const Cx<T>* src = a.sin[f] + noff + sline;
       for (int i = lane; i < Kz1 * nl; i += 32) {
         const int k = i / nl, l = i - (i / nl) * nl;
-        __pipeline_memcpy_async(st + ff * Kz1 * S::LPW + k * S::LPW + l, src + k * kzs + l, sizeof(Cx<T>));
+        __pipeline_memcpy_async(st + ff * fstride + k * S::LPW + l, src + k * kzs + l, sizeof(Cx<T>));
       }
     }
     __pipeline_commit();
   };
+  T sv1[S::R2], sv2[S::R2];
   prefetch(0);
   for (int q = 0; q < total; ++q) {
     if (q + 1 < total) {
@@ -392,22 +446,14 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
     const int node = q / npair, p = q - node * npair;
     const int f = 2 * p;
     const bool two = f + 1 < ns_blk;
-    const Cx<T>* st1 = stage + (q & 1) * 2 * Kz1 * S::LPW;
-    const Cx<T>* st2 = st1 + Kz1 * S::LPW;
-    auto load = [&](int line, int k) -> Cx<T> {
-      if (k == 0) return cx<T>(st1[line].x, two ? st2[line].x : (T)0);
-      if (k <= K2) {
-        const Cx<T> F1 = st1[k * S::LPW + line];
-        const Cx<T> F2 = two ? st2[k * S::LPW + line] : cx<T>(0, 0);
-        return cx<T>(F1.x - F2.y, F1.y + F2.x);
-      }
-      if (k >= L - K2) {
-        const int kk = L - k;
-        const Cx<T> F1 = st1[kk * S::LPW + line];
-        const Cx<T> F2 = two ? st2[kk * S::LPW + line] : cx<T>(0, 0);
-        return cx<T>(F1.x + F2.y, F2.x - F1.y);
-      }
-      return cx<T>(0, 0);
+    const Cx<T>* st1 = stage + (q & 1) * 2 * fstride;
+    const Cx<T>* st2 = st1 + fstride;
+    auto load = [&](int line, int, int n1) -> Cx<T> {
+      // branch-free Hermitian packing of F1 + i F2 (zero rows index the zero pad row)
+      const Cx<T> F1 = st1[hidx[n1] + line];
+      const Cx<T> F2 = st2[hidx[n1] + line];
+      const T sg = (T)hsg[n1];
+      return cx<T>(F1.x - sg * F2.y, sg * F1.y + F2.x);
     };
     auto store = [&](int line, int z, int k2, Cx<T> v) {
       const int li = line * L + z;
@@ -435,17 +481,36 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
           a.wout[f][gi] = v.x;
           if (two) a.wout[f + 1][gi] = v.y;
         }
-        const int o1 = a.oi[f], o2 = two ? a.oi[f + 1] : -1;
-        const T c1 = (T)a.sg[f] * v.x * Vst[a.ri[f] * ldR + li];
-        const T c2 = two ? (T)a.sg[f + 1] * v.y * Vst[a.ri[f + 1] * ldR + li] : (T)0;
-#pragma unroll
-        for (int o = 0; o < NOM; ++o) {
-          if (o == o1) acc[o][k2] += c1;
-          if (o == o2) acc[o][k2] += c2;
-        }
+        sv1[k2] = v.x;
+        sv2[k2] = v.y;
       }
     };
     wfft<T, S, true>(tile, tw, nl, load, store);
+    if constexpr (Tr::acc && OP != kOpContract) {
+      // uniform (per pair) output selection, then unrolled accumulation
+      if (own) {
+        const int o1 = a.oi[f], r1 = a.ri[f];
+        const T sg1 = (T)a.sg[f];
+        const T* V1 = Vst + r1 * ldR + bl * L + k1;
+#pragma unroll
+        for (int o = 0; o < NOM; ++o)
+          if (o == o1) {
+#pragma unroll
+            for (int k2 = 0; k2 < S::R2; ++k2) acc[o][k2] += sg1 * sv1[k2] * V1[S::R1 * k2];
+          }
+        if (two) {
+          const int o2 = a.oi[f + 1], r2 = a.ri[f + 1];
+          const T sg2 = (T)a.sg[f + 1];
+          const T* V2 = Vst + r2 * ldR + bl * L + k1;
+#pragma unroll
+          for (int o = 0; o < NOM; ++o)
+            if (o == o2) {
+#pragma unroll
+              for (int k2 = 0; k2 < S::R2; ++k2) acc[o][k2] += sg2 * sv2[k2] * V2[S::R1 * k2];
+            }
+        }
+      }
+    }
   }
   if constexpr (OP == kOpRealize) return;
   const int no = a.no;
@@ -466,7 +531,7 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
       }
       __syncwarp();
     }
-    auto load = [&](int line, int z) -> Cx<T> {
+    auto load = [&](int line, int z, int) -> Cx<T> {
       if constexpr (Tr::acc) {
         return xbuf[line * L + z];
       } else {
@@ -496,26 +561,33 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
 // forward y pass: S [o][kz][x][y] -> I [o][kz][ky][x] (band ky kept)
 // ---------------------------------------------------------------------------
 template <typename T, class S>
-__global__ void __launch_bounds__(kWarps * 32) k_yfwd(const Cx<T>* __restrict__ in, Cx<T>* __restrict__ out,
-                                                       PadGeom g, const double2* __restrict__ twg) {
+__global__ void __launch_bounds__(kPW * 32) k_yfwd(const Cx<T>* __restrict__ in, Cx<T>* __restrict__ out,
+                                                   PadGeom g, const double2* __restrict__ twg) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Cx<T>* tw = (Cx<T>*)smem_raw;
-  Cx<T>* tile = tw + S::L + (threadIdx.x >> 5) * S::TILE;
-  constexpr int LPC = kWarps * S::LPW;
+  constexpr int LPC = kPW * S::LPW;
   const int P0 = g.P[0], K1 = g.K[1], B1 = g.B[1];
+  Cx<T>* tw = (Cx<T>*)smem_raw;
+  Cx<T>* slab = tw + S::L;                       // [LPC][L]
+  Cx<T>* tile = slab + LPC * S::L + (threadIdx.x >> 5) * S::TILE;
   const int nxb = (P0 + LPC - 1) / LPC;
   const int per = g.Kz1 * nxb;
   const int f = blockIdx.x / per;
   const int r = blockIdx.x - f * per;
   const int kz = r / nxb;
-  const int x0 = (r - kz * nxb) * LPC + (threadIdx.x >> 5) * S::LPW;
+  const int cx0 = (r - kz * nxb) * LPC;
+  const int nlc = min(LPC, P0 - cx0);
+  const Cx<T>* src = in + f * g.ns + ((int64_t)kz * P0 + cx0) * S::L;  // nlc contiguous rows
+  for (int i = threadIdx.x; i < nlc * S::L; i += blockDim.x) cp_async<T>(slab + i, src + i);
+  __pipeline_commit();
   load_tw<T>(tw, twg, S::L);
+  __pipeline_wait_prior(0);
   __syncthreads();
-  const int nl = min(S::LPW, P0 - x0);
+  const int wl0 = (threadIdx.x >> 5) * S::LPW;
+  const int nl = min(S::LPW, nlc - wl0);
   if (nl <= 0) return;
-  const Cx<T>* src = in + f * g.ns + ((int64_t)kz * P0 + x0) * S::L;
-  Cx<T>* dst = out + f * g.n1 + (int64_t)kz * B1 * P0 + x0;
-  auto load = [&](int line, int y) -> Cx<T> { return src[line * S::L + y]; };
+  Cx<T>* dst = out + f * g.n1 + (int64_t)kz * B1 * P0 + cx0 + wl0;
+  const Cx<T>* sl = slab + wl0 * S::L;
+  auto load = [&](int line, int y, int) -> Cx<T> { return sl[line * S::L + y]; };
   auto store = [&](int line, int q, int, Cx<T> v) {
     const int iy = bin_to_index(q, S::L, K1, B1);
     if (iy >= 0) dst[iy * P0 + line] = v;
@@ -587,23 +659,34 @@ __device__ __forceinline__ void epilogue(const FwdArgs<T>& a, const FwdOut<T>& O
 }
 
 template <typename T, class S>
-__global__ void __launch_bounds__(kWarps * 32) k_xfwd(FwdArgs<T> a, PadGeom g, const double2* __restrict__ twg) {
+__global__ void __launch_bounds__(kPW * 32) k_xfwd(FwdArgs<T> a, PadGeom g, const double2* __restrict__ twg, int ntmax) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Cx<T>* tw = (Cx<T>*)smem_raw;
-  Cx<T>* tile = tw + S::L + (threadIdx.x >> 5) * S::TILE;
-  constexpr int LPC = kWarps * S::LPW;
+  constexpr int LPC = kPW * S::LPW;
   const int K0 = g.K[0], B0 = g.B[0], B1 = g.B[1];
+  Cx<T>* tw = (Cx<T>*)smem_raw;
+  Cx<T>* slab = tw + S::L;                       // [ntmax][LPC][L]
+  Cx<T>* tile = slab + ntmax * LPC * S::L + (threadIdx.x >> 5) * S::TILE;
   const int nyb = (B1 + LPC - 1) / LPC;
   const int per = g.Kz1 * nyb;
   const int o = blockIdx.x / per;
   const int r = blockIdx.x - o * per;
   const int kz = r / nyb;
-  const int ky0 = (r - kz * nyb) * LPC + (threadIdx.x >> 5) * S::LPW;
-  load_tw<T>(tw, twg, S::L);
-  __syncthreads();
-  const int nl = min(S::LPW, B1 - ky0);
-  if (nl <= 0) return;
+  const int cky0 = (r - kz * nyb) * LPC;
+  const int nlc = min(LPC, B1 - cky0);
   const FwdOut<T>& O = a.o[o];
+  for (int t = 0; t < O.nterms; ++t) {
+    const Cx<T>* src = a.in + O.f[t] * g.n1 + ((int64_t)kz * B1 + cky0) * S::L;  // nlc contiguous rows
+    Cx<T>* dst = slab + t * LPC * S::L;
+    for (int i = threadIdx.x; i < nlc * S::L; i += blockDim.x) cp_async<T>(dst + i, src + i);
+  }
+  __pipeline_commit();
+  load_tw<T>(tw, twg, S::L);
+  __pipeline_wait_prior(0);
+  __syncthreads();
+  const int wl0 = (threadIdx.x >> 5) * S::LPW;
+  const int nl = min(S::LPW, nlc - wl0);
+  if (nl <= 0) return;
+  const int ky0 = cky0 + wl0;
   const T kzk = (T)(kTwoPi * (double)kz);
   Cx<T> acc[S::R2];
 #pragma unroll
@@ -612,9 +695,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_xfwd(FwdArgs<T> a, PadGeom g, c
   const int bline = lane / S::R1;
   const int k1 = lane - bline * S::R1;
   for (int t = 0; t < O.nterms; ++t) {
-    const Cx<T>* src = a.in + O.f[t] * g.n1 + ((int64_t)kz * B1 + ky0) * S::L;
+    const Cx<T>* sl = slab + (t * LPC + wl0) * S::L;
     const int ax = O.axis[t];
-    auto load = [&](int line, int x) -> Cx<T> { return src[line * S::L + x]; };
+    auto load = [&](int line, int x, int) -> Cx<T> { return sl[line * S::L + x]; };
     auto store = [&](int line, int q, int k2, Cx<T> v) {
       const int ix = bin_to_index(q, S::L, K0, B0);
       if (ix < 0) return;
@@ -720,21 +803,23 @@ static void ensure_smem(K kernel, size_t bytes) {
 template <typename T, class S>
 void launch_xinv(blr_ctx* c, PadEngine* e, const XPassArgs<T>& a) {
   const PadGeom& g = e->g;
-  constexpr int LPC = kWarps * S::LPW;
-  const size_t sm = sizeof(Cx<T>) * (S::L + kWarps * S::TILE);
+  constexpr int LPC = kPW * S::LPW;
+  const size_t sm = sizeof(Cx<T>) * (S::L + (size_t)g.B[0] * LPC + kPW * S::TILE);
   ensure_smem(k_xinv<T, S>, sm);
   const int nyb = (g.B[1] + LPC - 1) / LPC;
-  k_xinv<T, S><<<a.nx * g.Kz1 * nyb, kWarps * 32, sm, c->stream>>>(a, g, e->tw[0]);
+  k_xinv<T, S><<<a.nx * g.Kz1 * nyb, kPW * 32, sm, c->stream>>>(a, g, e->tw[0]);
   BLR_LAUNCHED();
 }
 template <typename T, class S>
 void launch_yinv(blr_ctx* c, PadEngine* e, const YPassArgs<T>& a) {
   const PadGeom& g = e->g;
-  constexpr int LPC = kWarps * S::LPW;
-  const size_t sm = sizeof(Cx<T>) * (S::L + kWarps * S::TILE);
+  constexpr int LPC = kPW * S::LPW;
+  int ntmax = 1;
+  for (int i = 0; i < a.ny; ++i) ntmax = std::max(ntmax, a.nterms[i]);
+  const size_t sm = sizeof(Cx<T>) * (S::L + (size_t)ntmax * g.B[1] * LPC + kPW * S::TILE);
   ensure_smem(k_yinv<T, S>, sm);
   const int nxb = (g.P[0] + LPC - 1) / LPC;
-  k_yinv<T, S><<<a.ny * g.Kz1 * nxb, kWarps * 32, sm, c->stream>>>(a, g, e->tw[1]);
+  k_yinv<T, S><<<a.ny * g.Kz1 * nxb, kPW * 32, sm, c->stream>>>(a, g, e->tw[1], ntmax);
   BLR_LAUNCHED();
 }
 template <typename T, class S, int OP>
@@ -743,7 +828,7 @@ void launch_lines(blr_ctx* c, PadEngine* e, const LineArgs<T>& a) {
   const int ns_blk = OP == kOpContract ? a.d : a.ns;
   const int nreal = (ZOp<OP>::acc || OP == kOpRealize) ? 0 : ns_blk;
   const int nst = ZOp<OP>::acc ? a.nst : 0;
-  const size_t stage_n = std::max<size_t>(4 * (size_t)g.Kz1 * S::LPW, (size_t)S::LPW * S::L);
+  const size_t stage_n = std::max<size_t>(4 * (size_t)(g.Kz1 + 1) * S::LPW, (size_t)S::LPW * S::L);
   const size_t warp_bytes = sizeof(Cx<T>) * ((size_t)S::TILE + stage_n) +
                             sizeof(T) * (size_t)(nreal + nst) * S::LPW * S::L;
   const size_t sm = S::L * sizeof(Cx<T>) + kZWarps * warp_bytes;
@@ -761,21 +846,23 @@ void launch_lines(blr_ctx* c, PadEngine* e, const LineArgs<T>& a) {
 template <typename T, class S>
 void launch_yfwd(blr_ctx* c, PadEngine* e, const Cx<T>* in, int nf, Cx<T>* out) {
   const PadGeom& g = e->g;
-  constexpr int LPC = kWarps * S::LPW;
-  const size_t sm = sizeof(Cx<T>) * (S::L + kWarps * S::TILE);
+  constexpr int LPC = kPW * S::LPW;
+  const size_t sm = sizeof(Cx<T>) * (S::L + (size_t)LPC * S::L + kPW * S::TILE);
   ensure_smem(k_yfwd<T, S>, sm);
   const int nxb = (g.P[0] + LPC - 1) / LPC;
-  k_yfwd<T, S><<<nf * g.Kz1 * nxb, kWarps * 32, sm, c->stream>>>(in, out, g, e->tw[1]);
+  k_yfwd<T, S><<<nf * g.Kz1 * nxb, kPW * 32, sm, c->stream>>>(in, out, g, e->tw[1]);
   BLR_LAUNCHED();
 }
 template <typename T, class S>
 void launch_xfwd(blr_ctx* c, PadEngine* e, const FwdArgs<T>& a) {
   const PadGeom& g = e->g;
-  constexpr int LPC = kWarps * S::LPW;
-  const size_t sm = sizeof(Cx<T>) * (S::L + kWarps * S::TILE);
+  constexpr int LPC = kPW * S::LPW;
+  int ntmax = 1;
+  for (int i = 0; i < a.no; ++i) ntmax = std::max(ntmax, a.o[i].nterms);
+  const size_t sm = sizeof(Cx<T>) * (S::L + (size_t)ntmax * LPC * S::L + kPW * S::TILE);
   ensure_smem(k_xfwd<T, S>, sm);
   const int nyb = (g.B[1] + LPC - 1) / LPC;
-  k_xfwd<T, S><<<a.no * g.Kz1 * nyb, kWarps * 32, sm, c->stream>>>(a, g, e->tw[0]);
+  k_xfwd<T, S><<<a.no * g.Kz1 * nyb, kPW * 32, sm, c->stream>>>(a, g, e->tw[0], ntmax);
   BLR_LAUNCHED();
 }
 
