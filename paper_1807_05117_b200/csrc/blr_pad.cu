@@ -45,6 +45,8 @@ void pad_engine_release(blr_ctx* c) {
   if (it == engines().end()) return;
   for (auto* p : it->second.tw)
     if (p) cudaFree(p);
+  for (auto* p : it->second.buf)
+    if (p) cudaFree(p);
   engines().erase(it);
 }
 
@@ -91,6 +93,11 @@ static PadEngine* engine(blr_ctx* c) {
 
 template <typename T>
 bool pad_engine_ok(blr_ctx* c) { return engine<T>(c) != nullptr; }
+
+// persistent, grow-only per-engine scratch buffers (stream-ordered users only)
+static void* e_scratch(blr_ctx* c, PadEngine* e, int slot, size_t bytes) {
+  return scratch(c, e->buf[slot], e->buf_bytes[slot], bytes);
+}
 
 template <typename T>
 static void dispatch_xinv(blr_ctx* c, PadEngine* e, const XPassArgs<T>& a) {
@@ -171,8 +178,7 @@ static void inv2d(blr_ctx* c, PadEngine* e, const std::vector<InvSpec<T>>& f, Cx
       yx[i][t] = idx;
     }
   if ((int)xf.size() > kMaxX) throw Error(1, "too many x-pass fields");
-  Cx<T>* I = nullptr;
-  BLR_CUDA(cudaMallocAsync((void**)&I, xf.size() * g.n1 * sizeof(Cx<T>), c->stream));
+  Cx<T>* I = (Cx<T>*)e_scratch(c, e, 0, xf.size() * g.n1 * sizeof(Cx<T>));
   {
     XPassArgs<T> a;
     std::memset(&a, 0, sizeof(a));
@@ -201,7 +207,6 @@ static void inv2d(blr_ctx* c, PadEngine* e, const std::vector<InvSpec<T>>& f, Cx
     ProfScope ps(c, "pad_ypass", ((double)nterm * g.n1 + a.ny * g.ns) * sizeof(Cx<T>));
     dispatch_yinv<T>(c, e, a);
   }
-  BLR_CUDA(cudaFreeAsync(I, c->stream));
 }
 
 // --- z lines -------------------------------------------------------------------------
@@ -279,8 +284,7 @@ static void fwd2d(blr_ctx* c, PadEngine* e, const std::vector<FwdSpec<T>>& outs,
       if (idx < 0) { idx = (int)sf.size(); sf.push_back(outs[i].sin[t]); }
       fi[i][t] = idx;
     }
-  Cx<T>* I = nullptr;
-  BLR_CUDA(cudaMallocAsync((void**)&I, sf.size() * g.n1 * sizeof(Cx<T>), c->stream));
+  Cx<T>* I = (Cx<T>*)e_scratch(c, e, 1, sf.size() * g.n1 * sizeof(Cx<T>));
   {
     size_t i = 0;
     while (i < sf.size()) {
@@ -292,8 +296,7 @@ static void fwd2d(blr_ctx* c, PadEngine* e, const std::vector<FwdSpec<T>>& outs,
       i = j;
     }
   }
-  Cx<T>* z0 = nullptr;
-  BLR_CUDA(cudaMallocAsync((void**)&z0, outs.size() * (size_t)g.B[0] * g.B[1] * sizeof(Cx<T>), c->stream));
+  Cx<T>* z0 = (Cx<T>*)e_scratch(c, e, 2, outs.size() * (size_t)g.B[0] * g.B[1] * sizeof(Cx<T>));
   for (size_t off = 0; off < outs.size(); off += kMaxFwd) {
     FwdArgs<T> a;
     std::memset(&a, 0, sizeof(a));
@@ -329,8 +332,6 @@ static void fwd2d(blr_ctx* c, PadEngine* e, const std::vector<FwdSpec<T>>& outs,
     k_fix0<T><<<grid_blocks(n0, 256), 256, 0, c->stream>>>(a, g);
     BLR_LAUNCHED();
   }
-  BLR_CUDA(cudaFreeAsync(z0, c->stream));
-  BLR_CUDA(cudaFreeAsync(I, c->stream));
 }
 
 template <typename T>

@@ -434,6 +434,18 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
     __pipeline_commit();
   };
   T sv1[S::R2], sv2[S::R2];
+  // Outer: V_j at this lane's step-A positions (line la, z = R2*n1 + n2), used by every R2C gather
+  T vreg[OP == kOpOuter ? 3 : 1][OP == kOpOuter ? S::R1 : 1];
+  if constexpr (OP == kOpOuter) {
+    const int la = lane / S::R2, n2a = lane - (lane / S::R2) * S::R2;
+    const bool oka = la < nl && la < S::LPW;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const T* vj = a.rin[j < a.d ? j : 0] + rline + (oka ? la : 0) * L + n2a;
+#pragma unroll
+      for (int n1 = 0; n1 < S::R1; ++n1) vreg[j][n1] = oka ? __ldg(vj + S::R2 * n1) : (T)0;
+    }
+  }
   prefetch(0);
   for (int q = 0; q < total; ++q) {
     if (q + 1 < total) {
@@ -531,9 +543,20 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
       }
       __syncwarp();
     }
-    auto load = [&](int line, int z, int) -> Cx<T> {
+    auto load = [&](int line, int z, int n1) -> Cx<T> {
       if constexpr (Tr::acc) {
         return xbuf[line * L + z];
+      } else if constexpr (OP == kOpOuter) {
+        const int d = a.d, li = line * L + z;
+        const int i1 = o / d, j1 = o - i1 * d;
+        const T v1 = j1 == 0 ? vreg[0][n1] : (j1 == 1 ? vreg[1][n1] : vreg[2][n1]);
+        T r2 = 0;
+        if (two) {
+          const int i2 = (o + 1) / d, j2 = o + 1 - i2 * d;
+          const T v2 = j2 == 0 ? vreg[0][n1] : (j2 == 1 ? vreg[1][n1] : vreg[2][n1]);
+          r2 = Rsm[i2 * ldR + li] * v2;
+        }
+        return cx<T>(Rsm[i1 * ldR + li] * v1, r2);
       } else {
         const int li = line * L + z;
         const int64_t gi = rline + li;
@@ -792,12 +815,22 @@ struct PadEngine {
   PadGeom g{};
   double2* tw[3] = {nullptr, nullptr, nullptr};
   int line_smem_max = 0;
+  void* buf[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t buf_bytes[4] = {0, 0, 0, 0};
 };
 
 
+// raise the kernel's dynamic shared-memory limit once (not per launch)
 template <class K>
 static void ensure_smem(K kernel, size_t bytes) {
-  if (bytes > 48 * 1024) BLR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  static size_t set = 48 * 1024;  // one static per kernel instantiation
+  if (bytes > set) {
+    int dev, maxsm;
+    BLR_CUDA(cudaGetDevice(&dev));
+    BLR_CUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    BLR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+    set = (size_t)maxsm;
+  }
 }
 
 template <typename T, class S>
