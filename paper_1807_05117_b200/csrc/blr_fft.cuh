@@ -364,14 +364,20 @@ struct WShape {
 
 // step A: lanes (line, n2) gather x[R2*n1 + n2] with load(line, n, n1), DFT_R1,
 // twiddle W_L^(n2 k1) (table tw[m] = exp(-2 pi i m / L)), store to the tile.
-template <typename T, class S, bool INV, class Load>
+// ALIAS: the tile overlays the warp's own input lines in shared memory, so all
+// lanes finish loading before any lane stores.
+template <typename T, class S, bool INV, bool ALIAS = false, class Load>
 __device__ __forceinline__ void wfft_a(Cx<T>* tile, const Cx<T>* tw, int nl, Load& load) {
   const int lane = threadIdx.x & 31;
   const int line = lane / S::R2, n2 = lane - (lane / S::R2) * S::R2;
-  if (line < nl && line < S::LPW) {
-    Cx<T> v[S::R1];
+  const bool act = line < nl && line < S::LPW;
+  Cx<T> v[S::R1];
+  if (act) {
 #pragma unroll
     for (int n1 = 0; n1 < S::R1; ++n1) v[n1] = load(line, S::R2 * n1 + n2, n1);
+  }
+  if (ALIAS) __syncwarp();
+  if (act) {
     dft<T, S::R1, INV>(v);
     Cx<T>* t = tile + line * S::TS + n2;
 #pragma unroll
@@ -406,9 +412,9 @@ __device__ __forceinline__ void wfft_b(const Cx<T>* tile, int nl, Store& store) 
   __syncwarp();
 }
 
-template <typename T, class S, bool INV, class Load, class Store>
+template <typename T, class S, bool INV, bool ALIAS = false, class Load, class Store>
 __device__ __forceinline__ void wfft(Cx<T>* tile, const Cx<T>* tw, int nl, Load load, Store store) {
-  wfft_a<T, S, INV>(tile, tw, nl, load);
+  wfft_a<T, S, INV, ALIAS>(tile, tw, nl, load);
   wfft_b<T, S, INV>(tile, nl, store);
 }
 

@@ -15,8 +15,8 @@ namespace blr {
   extern template void launch_xinv<float, WShape<A, B>>(blr_ctx*, PadEngine*, const XPassArgs<float>&);   \
   extern template void launch_yinv<double, WShape<A, B>>(blr_ctx*, PadEngine*, const YPassArgs<double>&); \
   extern template void launch_yinv<float, WShape<A, B>>(blr_ctx*, PadEngine*, const YPassArgs<float>&);   \
-  extern template void launch_yfwd<double, WShape<A, B>>(blr_ctx*, PadEngine*, const double2*, int, double2*); \
-  extern template void launch_yfwd<float, WShape<A, B>>(blr_ctx*, PadEngine*, const float2*, int, float2*);    \
+  extern template void launch_yfwd<double, WShape<A, B>>(blr_ctx*, PadEngine*, const YFwdArgs<double>&); \
+  extern template void launch_yfwd<float, WShape<A, B>>(blr_ctx*, PadEngine*, const YFwdArgs<float>&);   \
   extern template void launch_xfwd<double, WShape<A, B>>(blr_ctx*, PadEngine*, const FwdArgs<double>&);   \
   extern template void launch_xfwd<float, WShape<A, B>>(blr_ctx*, PadEngine*, const FwdArgs<float>&);
 BLR_FOR_EACH_L(BLR_EXTERN_L)
@@ -127,9 +127,9 @@ static void dispatch_lines(blr_ctx* c, PadEngine* e, const LineArgs<T>& a) {
   }
 }
 template <typename T>
-static void dispatch_yfwd(blr_ctx* c, PadEngine* e, const Cx<T>* in, int nf, Cx<T>* out) {
+static void dispatch_yfwd(blr_ctx* c, PadEngine* e, const YFwdArgs<T>& a) {
   switch (e->g.P[1]) {
-#define X(LL, A, B) case LL: launch_yfwd<T, WShape<A, B>>(c, e, in, nf, out); break;
+#define X(LL, A, B) case LL: launch_yfwd<T, WShape<A, B>>(c, e, a); break;
     BLR_FOR_EACH_L(X)
 #undef X
     default: throw Error(1, "unsupported pad length");
@@ -274,27 +274,51 @@ struct Rk {
 template <typename T>
 static void fwd2d(blr_ctx* c, PadEngine* e, const std::vector<FwdSpec<T>>& outs, Cx<T>* kout, const Rk& rk) {
   const PadGeom& g = e->g;
-  std::vector<const Cx<T>*> sf;
-  std::vector<std::array<int, 3>> fi(outs.size());
-  for (size_t i = 0; i < outs.size(); ++i)
+  // forward-y jobs: x-derivative terms stay separate (i k_x after the x pass);
+  // the other terms of an output (plain, i k_y, i k_z) fold into one job
+  struct Job { int nt; const Cx<T>* s[3]; int ax[3]; };
+  std::vector<Job> jobs;
+  struct XT { int nt; int f[3]; int ax[3]; };
+  std::vector<XT> xt(outs.size());
+  for (size_t i = 0; i < outs.size(); ++i) {
+    xt[i].nt = 0;
+    Job comb{};
     for (int t = 0; t < outs[i].nterms; ++t) {
-      int idx = -1;
-      for (size_t q = 0; q < sf.size(); ++q)
-        if (sf[q] == outs[i].sin[t]) { idx = (int)q; break; }
-      if (idx < 0) { idx = (int)sf.size(); sf.push_back(outs[i].sin[t]); }
-      fi[i][t] = idx;
+      if (outs[i].axis[t] == 0) {
+        Job jx{};
+        jx.nt = 1; jx.s[0] = outs[i].sin[t]; jx.ax[0] = -1;
+        jobs.push_back(jx);
+        xt[i].f[xt[i].nt] = (int)jobs.size() - 1;
+        xt[i].ax[xt[i].nt++] = 0;
+      } else {
+        comb.s[comb.nt] = outs[i].sin[t];
+        comb.ax[comb.nt++] = outs[i].axis[t];
+      }
     }
-  Cx<T>* I = (Cx<T>*)e_scratch(c, e, 1, sf.size() * g.n1 * sizeof(Cx<T>));
-  {
-    size_t i = 0;
-    while (i < sf.size()) {
-      size_t j = i + 1;
-      while (j < sf.size() && sf[j] == sf[i] + (int64_t)(j - i) * g.ns) ++j;
-      const int nf = (int)(j - i);
-      ProfScope ps(c, "pad_ypass_fwd", (double)nf * (g.ns + g.n1) * sizeof(Cx<T>));
-      dispatch_yfwd<T>(c, e, sf[i], nf, I + (int64_t)i * g.n1);
-      i = j;
+    if (comb.nt) {
+      jobs.push_back(comb);
+      xt[i].f[xt[i].nt] = (int)jobs.size() - 1;
+      xt[i].ax[xt[i].nt++] = -1;
     }
+  }
+  Cx<T>* I = (Cx<T>*)e_scratch(c, e, 1, jobs.size() * g.n1 * sizeof(Cx<T>));
+  for (size_t off = 0; off < jobs.size(); off += kMaxYF) {
+    YFwdArgs<T> a;
+    std::memset(&a, 0, sizeof(a));
+    a.nj = (int)std::min<size_t>(kMaxYF, jobs.size() - off);
+    int nterm = 0;
+    for (int q = 0; q < a.nj; ++q) {
+      const Job& jb = jobs[off + q];
+      a.nterms[q] = jb.nt;
+      for (int t = 0; t < 3; ++t) {
+        a.sin[q][t] = t < jb.nt ? jb.s[t] : jb.s[0];
+        a.axis[q][t] = t < jb.nt ? jb.ax[t] : -1;
+      }
+      nterm += jb.nt;
+    }
+    a.out = I + (int64_t)off * g.n1;
+    ProfScope ps(c, "pad_ypass_fwd", ((double)nterm * g.ns + a.nj * g.n1) * sizeof(Cx<T>));
+    dispatch_yfwd<T>(c, e, a);
   }
   Cx<T>* z0 = (Cx<T>*)e_scratch(c, e, 2, outs.size() * (size_t)g.B[0] * g.B[1] * sizeof(Cx<T>));
   for (size_t off = 0; off < outs.size(); off += kMaxFwd) {
@@ -304,14 +328,15 @@ static void fwd2d(blr_ctx* c, PadEngine* e, const std::vector<FwdSpec<T>>& outs,
     int nterm = 0;
     for (int i = 0; i < a.no; ++i) {
       const FwdSpec<T>& s = outs[off + i];
+      const XT& x = xt[off + i];
       for (int t = 0; t < 3; ++t) {
-        a.o[i].f[t] = t < s.nterms ? fi[off + i][t] : 0;
-        a.o[i].axis[t] = s.axis[t];
+        a.o[i].f[t] = t < x.nt ? x.f[t] : 0;
+        a.o[i].axis[t] = t < x.nt ? x.ax[t] : -1;
       }
-      a.o[i].nterms = s.nterms;
+      a.o[i].nterms = x.nt;
       a.o[i].mode = s.mode;
       a.o[i].vt = s.vt;
-      nterm += s.nterms;
+      nterm += x.nt;
     }
     a.in = I;
     a.scale = (T)(1.0 / (double)g.np);

@@ -5,7 +5,7 @@
 namespace blr {
 template void launch_xinv<double, WShape<7, 7>>(blr_ctx*, PadEngine*, const XPassArgs<double>&);
 template void launch_yinv<double, WShape<7, 7>>(blr_ctx*, PadEngine*, const YPassArgs<double>&);
-template void launch_yfwd<double, WShape<7, 7>>(blr_ctx*, PadEngine*, const double2*, int, double2*);
+template void launch_yfwd<double, WShape<7, 7>>(blr_ctx*, PadEngine*, const YFwdArgs<double>&);
 template void launch_xfwd<double, WShape<7, 7>>(blr_ctx*, PadEngine*, const FwdArgs<double>&);
 template void launch_lines<double, WShape<7, 7>, 0>(blr_ctx*, PadEngine*, const LineArgs<double>&);
 template void launch_lines<double, WShape<7, 7>, 1>(blr_ctx*, PadEngine*, const LineArgs<double>&);
@@ -18,7 +18,7 @@ template void launch_lines<double, WShape<7, 7>, 7>(blr_ctx*, PadEngine*, const 
 template void launch_lines<double, WShape<7, 7>, 8>(blr_ctx*, PadEngine*, const LineArgs<double>&);
 template void launch_xinv<float, WShape<7, 7>>(blr_ctx*, PadEngine*, const XPassArgs<float>&);
 template void launch_yinv<float, WShape<7, 7>>(blr_ctx*, PadEngine*, const YPassArgs<float>&);
-template void launch_yfwd<float, WShape<7, 7>>(blr_ctx*, PadEngine*, const float2*, int, float2*);
+template void launch_yfwd<float, WShape<7, 7>>(blr_ctx*, PadEngine*, const YFwdArgs<float>&);
 template void launch_xfwd<float, WShape<7, 7>>(blr_ctx*, PadEngine*, const FwdArgs<float>&);
 template void launch_lines<float, WShape<7, 7>, 0>(blr_ctx*, PadEngine*, const LineArgs<float>&);
 template void launch_lines<float, WShape<7, 7>, 1>(blr_ctx*, PadEngine*, const LineArgs<float>&);

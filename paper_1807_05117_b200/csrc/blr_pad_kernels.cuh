@@ -83,14 +83,54 @@ __device__ __forceinline__ void cp_async(Cx<T>* dst, const Cx<T>* src) {
 // its four-step FFTs from shared memory.
 constexpr int kPW = 4;
 
+// Shared-memory strides chosen so the FFT access patterns are free of bank
+// conflicts.  Transposed tiles [row][LPC] are read by lanes walking rows, so
+// their row stride is made odd.  Line slabs [line][L] are read by step-A lanes
+// (line, n2) at line*LS + n2 + const; LS = L + pad with the smallest pad whose
+// worst 128-byte phase maps no two lanes onto one bank.
+template <int LPC>
+constexpr int t_stride() { return LPC | 1; }
+
+template <class S>
+constexpr int phase_conflicts(int LS, int words) {
+  const int per_phase = 32 / words;  // lanes served per 128-byte wavefront
+  int worst = 0;
+  for (int p0 = 0; p0 < 32; p0 += per_phase) {
+    int cnt[32] = {};
+    for (int lane = p0; lane < p0 + per_phase; ++lane) {
+      const int line = lane / S::R2, n2 = lane % S::R2;
+      if (line >= S::LPW) continue;
+      const int w0 = (line * LS + n2) * words;
+      for (int w = 0; w < words; ++w) ++cnt[(w0 + w) % 32];
+    }
+    for (int b = 0; b < 32; ++b) worst = cnt[b] > worst ? cnt[b] : worst;
+  }
+  return worst;
+}
+
+// ALIAS: the slab must also hold the warp's FFT tile over its own lines
+// (LS >= TS), which drops the separate per-warp tiles.
+template <typename T, class S, bool ALIAS = false>
+constexpr int row_stride() {
+  constexpr int words = (int)(sizeof(Cx<T>) / 4);
+  const int base = ALIAS && S::TS > S::L ? S::TS : S::L;
+  int best = base, bc = phase_conflicts<S>(base, words);
+  for (int p = 1; p < 8; ++p) {
+    const int c = phase_conflicts<S>(base + p, words);
+    if (c < bc) { bc = c; best = base + p; }
+  }
+  return best;
+}
+
 template <typename T, class S>
 __global__ void __launch_bounds__(kPW * 32) k_xinv(XPassArgs<T> a, PadGeom g, const double2* __restrict__ twg) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int LPC = kPW * S::LPW;
   const int K0 = g.K[0], B0 = g.B[0], B1 = g.B[1];
   Cx<T>* tw = (Cx<T>*)smem_raw;
-  Cx<T>* slab = tw + S::L;                       // [B0][LPC]
-  Cx<T>* tile = slab + B0 * LPC + (threadIdx.x >> 5) * S::TILE;
+  constexpr int LPCS = t_stride<LPC>();
+  Cx<T>* slab = tw + S::L;                       // [B0][LPCS]
+  Cx<T>* tile = slab + B0 * LPCS + (threadIdx.x >> 5) * S::TILE;
   const int nyb = (B1 + LPC - 1) / LPC;
   const int per = g.Kz1 * nyb;
   const int xf = blockIdx.x / per;
@@ -101,7 +141,7 @@ __global__ void __launch_bounds__(kPW * 32) k_xinv(XPassArgs<T> a, PadGeom g, co
   const Cx<T>* src = a.src[xf] + ((int64_t)kz * B0) * B1 + cky0;
   for (int i = threadIdx.x; i < B0 * LPC; i += blockDim.x) {
     const int ix = i / LPC, l = i - ix * LPC;
-    if (l < nlc) cp_async<T>(slab + i, src + ix * B1 + l);
+    if (l < nlc) cp_async<T>(slab + ix * LPCS + l, src + ix * B1 + l);
   }
   __pipeline_commit();
   load_tw<T>(tw, twg, S::L);
@@ -116,7 +156,7 @@ __global__ void __launch_bounds__(kPW * 32) k_xinv(XPassArgs<T> a, PadGeom g, co
     const int ix = bin_to_index(p, S::L, K0, B0);
     const bool ok = ix >= 0;
     const int ixc = ok ? ix : 0;
-    Cx<T> z = slab[ixc * LPC + wl0 + line];
+    Cx<T> z = slab[ixc * LPCS + wl0 + line];
     if (mulx) z = mul_ik<T>(z, (T)(kTwoPi * (double)freq_of(ixc, K0, B0)));
     return ok ? z : cx<T>(0, 0);
   };
@@ -143,8 +183,9 @@ __global__ void __launch_bounds__(kPW * 32) k_yinv(YPassArgs<T> a, PadGeom g, co
   constexpr int LPC = kPW * S::LPW;
   const int P0 = g.P[0], K1 = g.K[1], B1 = g.B[1];
   Cx<T>* tw = (Cx<T>*)smem_raw;
-  Cx<T>* slab = tw + S::L;                       // [ntmax][B1][LPC]
-  Cx<T>* tile = slab + ntmax * B1 * LPC + (threadIdx.x >> 5) * S::TILE;
+  constexpr int LPCS = t_stride<LPC>();
+  Cx<T>* slab = tw + S::L;                       // [ntmax][B1][LPCS]
+  Cx<T>* tile = slab + ntmax * B1 * LPCS + (threadIdx.x >> 5) * S::TILE;
   const int nxb = (P0 + LPC - 1) / LPC;
   const int per = g.Kz1 * nxb;
   const int yf = blockIdx.x / per;
@@ -155,10 +196,10 @@ __global__ void __launch_bounds__(kPW * 32) k_yinv(YPassArgs<T> a, PadGeom g, co
   const int nt = a.nterms[yf];
   for (int t = 0; t < nt; ++t) {
     const Cx<T>* src = a.in + a.xf[yf][t] * g.n1 + (int64_t)kz * B1 * P0 + cx0;
-    Cx<T>* dst = slab + t * B1 * LPC;
+    Cx<T>* dst = slab + t * B1 * LPCS;
     for (int i = threadIdx.x; i < B1 * LPC; i += blockDim.x) {
       const int iy = i / LPC, l = i - iy * LPC;
-      if (l < nlc) cp_async<T>(dst + i, src + iy * P0 + l);
+      if (l < nlc) cp_async<T>(dst + iy * LPCS + l, src + iy * P0 + l);
     }
   }
   __pipeline_commit();
@@ -181,7 +222,7 @@ __global__ void __launch_bounds__(kPW * 32) k_yinv(YPassArgs<T> a, PadGeom g, co
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
       if (ax[t] < -1) break;
-      Cx<T> z = slab[(t * B1 + iyc) * LPC + wl0 + line];
+      Cx<T> z = slab[(t * B1 + iyc) * LPCS + wl0 + line];
       if (ax[t] >= 1) z = mul_ik<T>(z, ax[t] == 1 ? ky : kzk);
       acc = cadd(acc, z);
     }
@@ -243,7 +284,7 @@ template <int OP> struct ZOp {
   static constexpr int nomax = OP == kOpInvVol ? 4 : 3;
 };
 
-constexpr int kZWarps = 4;
+constexpr int kZWarps = 2;
 
 template <typename T, class S, int OP>
 __device__ __forceinline__ T z_output(const LineArgs<T>& a, const T* Rsm, int ldR, int li, int64_t gi, int o) {
@@ -583,39 +624,96 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
 // ---------------------------------------------------------------------------
 // forward y pass: S [o][kz][x][y] -> I [o][kz][ky][x] (band ky kept)
 // ---------------------------------------------------------------------------
+// A forward-y "job" produces one I field: sum_t m_t * Y(S_t), m_t = 1, i k_y
+// (after the transform) or i k_z.  Flux divergence folds its y and z terms
+// into one job; the x term needs i k_x after the x pass and stays separate.
+constexpr int kMaxYF = 24;
+template <typename T>
+struct YFwdArgs {
+  const Cx<T>* sin[kMaxYF][3];
+  int axis[kMaxYF][3];
+  int nterms[kMaxYF];
+  int nj;
+  Cx<T>* out;
+};
+
+// Persistent, double-buffered: each CTA walks items blockIdx.x + k*gridDim.x;
+// the cp.async slab of the next (item, term) load streams in while the warps
+// transform the current one, so HBM stays busy through the FFT phase.
 template <typename T, class S>
-__global__ void __launch_bounds__(kPW * 32) k_yfwd(const Cx<T>* __restrict__ in, Cx<T>* __restrict__ out,
-                                                   PadGeom g, const double2* __restrict__ twg) {
+__global__ void __launch_bounds__(kPW * 32, 4) k_yfwd(YFwdArgs<T> a, PadGeom g, const double2* __restrict__ twg) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int LPC = kPW * S::LPW;
+  constexpr int LS = row_stride<T, S, true>();
+  constexpr int LPCS = t_stride<LPC>();
+  constexpr int SLAB = LPC * LS;
   const int P0 = g.P[0], K1 = g.K[1], B1 = g.B[1];
   Cx<T>* tw = (Cx<T>*)smem_raw;
-  Cx<T>* slab = tw + S::L;                       // [LPC][L]
-  Cx<T>* tile = slab + LPC * S::L + (threadIdx.x >> 5) * S::TILE;
+  Cx<T>* slab = tw + S::L;                       // [2][LPC][LS]; each warp's FFT tile overlays its lines
+  Cx<T>* res = slab + 2 * SLAB;                  // [B1][LPCS] job accumulator
   const int nxb = (P0 + LPC - 1) / LPC;
   const int per = g.Kz1 * nxb;
-  const int f = blockIdx.x / per;
-  const int r = blockIdx.x - f * per;
-  const int kz = r / nxb;
-  const int cx0 = (r - kz * nxb) * LPC;
-  const int nlc = min(LPC, P0 - cx0);
-  const Cx<T>* src = in + f * g.ns + ((int64_t)kz * P0 + cx0) * S::L;  // nlc contiguous rows
-  for (int i = threadIdx.x; i < nlc * S::L; i += blockDim.x) cp_async<T>(slab + i, src + i);
-  __pipeline_commit();
-  load_tw<T>(tw, twg, S::L);
-  __pipeline_wait_prior(0);
-  __syncthreads();
-  const int wl0 = (threadIdx.x >> 5) * S::LPW;
-  const int nl = min(S::LPW, nlc - wl0);
-  if (nl <= 0) return;
-  Cx<T>* dst = out + f * g.n1 + (int64_t)kz * B1 * P0 + cx0 + wl0;
-  const Cx<T>* sl = slab + wl0 * S::L;
-  auto load = [&](int line, int y, int) -> Cx<T> { return sl[line * S::L + y]; };
-  auto store = [&](int line, int q, int, Cx<T> v) {
-    const int iy = bin_to_index(q, S::L, K1, B1);
-    if (iy >= 0) dst[iy * P0 + line] = v;
+  const int nitems = a.nj * per;
+  auto issue = [&](int it, int t, int b) {
+    const int jb = it / per;
+    const int r = it - jb * per;
+    const int kz = r / nxb;
+    const int cx0 = (r - kz * nxb) * LPC;
+    const int nlc = min(LPC, P0 - cx0);
+    const Cx<T>* src = a.sin[jb][t] + ((int64_t)kz * P0 + cx0) * S::L;  // nlc contiguous rows
+    Cx<T>* dst = slab + b * SLAB;
+    for (int i = threadIdx.x; i < nlc * S::L; i += blockDim.x) {
+      const int row = i / S::L;
+      cp_async<T>(dst + row * LS + (i - row * S::L), src + i);
+    }
   };
-  wfft<T, S, false>(tile, tw, nl, load, store);
+  load_tw<T>(tw, twg, S::L);
+  int it = blockIdx.x, t = 0, b = 0;
+  if (it < nitems) issue(it, 0, 0);
+  __pipeline_commit();
+  const int wl0 = (threadIdx.x >> 5) * S::LPW;
+  while (it < nitems) {
+    const int jb = it / per;
+    const int nt = a.nterms[jb];
+    int nit = it, ntt = t + 1;
+    if (ntt >= nt) { nit = it + gridDim.x; ntt = 0; }
+    if (nit < nitems) issue(nit, ntt, b ^ 1);
+    __pipeline_commit();
+    __pipeline_wait_prior(1);
+    __syncthreads();
+    const int r = it - jb * per;
+    const int kz = r / nxb;
+    const int cx0 = (r - kz * nxb) * LPC;
+    const int nl = min(S::LPW, min(LPC, P0 - cx0) - wl0);
+    if (nl > 0) {
+      const int ax = a.axis[jb][t];
+      const T kzk = (T)(kTwoPi * (double)kz);
+      const Cx<T>* sl = slab + b * SLAB + wl0 * LS;
+      auto load = [&](int line, int y, int) -> Cx<T> { return sl[line * LS + y]; };
+      auto store = [&](int line, int q, int, Cx<T> v) {
+        const int iy = bin_to_index(q, S::L, K1, B1);
+        if (iy < 0) return;
+        if (ax == 1) v = mul_ik<T>(v, (T)(kTwoPi * (double)freq_of(iy, K1, B1)));
+        else if (ax == 2) v = mul_ik<T>(v, kzk);
+        Cx<T>* rp = res + iy * LPCS + wl0 + line;  // owned by this lane for every term
+        *rp = t == 0 ? v : cadd(*rp, v);
+      };
+      wfft<T, S, false, true>(slab + b * SLAB + wl0 * LS, tw, nl, load, store);
+    }
+    if (t == nt - 1) {
+      __syncthreads();
+      const int nlc = min(LPC, P0 - cx0);
+      Cx<T>* dst = a.out + jb * g.n1 + (int64_t)kz * B1 * P0 + cx0;
+      for (int i = threadIdx.x; i < B1 * nlc; i += blockDim.x) {
+        const int iy = i / nlc, l = i - (i / nlc) * nlc;
+        dst[iy * P0 + l] = res[iy * LPCS + l];
+      }
+    }
+    __syncthreads();
+    it = nit;
+    t = ntt;
+    b ^= 1;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -681,69 +779,140 @@ __device__ __forceinline__ void epilogue(const FwdArgs<T>& a, const FwdOut<T>& O
   }
 }
 
+// Cooperative epilogue of one (output, kz, ky-chunk) block from the result
+// tile res[ix][LPCS]: consecutive threads take consecutive ky (coalesced), and
+// each thread issues the operand loads of U elements before any store, so the
+// RK4 read-modify-write costs one memory latency per U elements, not one each.
+template <typename T, int LPCS>
+__device__ __forceinline__ void epilogue_block(const FwdArgs<T>& a, const FwdOut<T>& O, int o, int kz,
+                                               int cky0, int nlc, const PadGeom& g, const Cx<T>* res) {
+  constexpr int U = 2;
+  const int B0 = g.B[0], B1 = g.B[1];
+  const int n = B0 * nlc;
+  const int s = a.rk_s;
+  for (int i0 = threadIdx.x; i0 < n; i0 += U * blockDim.x) {
+    Cx<T> r[U], v[U], cc[U], ac[U];
+    int64_t e[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i >= n) continue;
+      const int ix = i / nlc, l = i - (i / nlc) * nlc;
+      e[u] = ((int64_t)kz * B0 + ix) * B1 + cky0 + l;
+      r[u] = cscale(res[ix * LPCS + l], a.scale);
+      const int64_t h = (int64_t)o * g.nh + e[u];
+      if (O.mode == kEpiNegAdd) v[u] = O.vt[e[u]];
+      if (s) cc[u] = a.cur[h];
+      if (s > 1) ac[u] = a.acc[h];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i >= n) continue;
+      const int64_t h = (int64_t)o * g.nh + e[u];
+      Cx<T> k;
+      if (O.mode == kEpiNegAdd) k = cx<T>(-(v[u].x + r[u].x), -(v[u].y + r[u].y));
+      else if (O.mode == kEpiNeg) k = cx<T>(-r[u].x, -r[u].y);
+      else k = r[u];
+      if (a.kout) a.kout[h] = k;
+      if (s) {
+        Cx<T> acv;
+        if (s == 1) {
+          acv = k;
+        } else {
+          const T m = s < 4 ? (T)2 : (T)1;
+          acv = cx<T>(ac[u].x + m * k.x, ac[u].y + m * k.y);
+        }
+        if (s < 4) {
+          a.acc[h] = acv;
+          a.stage[h] = cx<T>(cc[u].x + a.cs * k.x, cc[u].y + a.cs * k.y);
+        } else {
+          a.cur[h] = cx<T>(cc[u].x + a.h6 * acv.x, cc[u].y + a.h6 * acv.y);
+        }
+      }
+    }
+  }
+}
+
 template <typename T, class S>
-__global__ void __launch_bounds__(kPW * 32) k_xfwd(FwdArgs<T> a, PadGeom g, const double2* __restrict__ twg, int ntmax) {
+__global__ void __launch_bounds__(kPW * 32, 3) k_xfwd(FwdArgs<T> a, PadGeom g, const double2* __restrict__ twg) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int LPC = kPW * S::LPW;
+  constexpr int LS = row_stride<T, S, true>();
+  constexpr int LPCS = t_stride<LPC>();
+  constexpr int SLAB = LPC * LS;
   const int K0 = g.K[0], B0 = g.B[0], B1 = g.B[1];
   Cx<T>* tw = (Cx<T>*)smem_raw;
-  Cx<T>* slab = tw + S::L;                       // [ntmax][LPC][L]
-  Cx<T>* tile = slab + ntmax * LPC * S::L + (threadIdx.x >> 5) * S::TILE;
+  Cx<T>* slab = tw + S::L;                       // [2][LPC][LS] (persistent, as k_yfwd)
+  Cx<T>* res = slab + 2 * SLAB;                  // [B0][LPCS] finished block
   const int nyb = (B1 + LPC - 1) / LPC;
   const int per = g.Kz1 * nyb;
-  const int o = blockIdx.x / per;
-  const int r = blockIdx.x - o * per;
-  const int kz = r / nyb;
-  const int cky0 = (r - kz * nyb) * LPC;
-  const int nlc = min(LPC, B1 - cky0);
-  const FwdOut<T>& O = a.o[o];
-  for (int t = 0; t < O.nterms; ++t) {
-    const Cx<T>* src = a.in + O.f[t] * g.n1 + ((int64_t)kz * B1 + cky0) * S::L;  // nlc contiguous rows
-    Cx<T>* dst = slab + t * LPC * S::L;
-    for (int i = threadIdx.x; i < nlc * S::L; i += blockDim.x) cp_async<T>(dst + i, src + i);
-  }
-  __pipeline_commit();
-  load_tw<T>(tw, twg, S::L);
-  __pipeline_wait_prior(0);
-  __syncthreads();
-  const int wl0 = (threadIdx.x >> 5) * S::LPW;
-  const int nl = min(S::LPW, nlc - wl0);
-  if (nl <= 0) return;
-  const int ky0 = cky0 + wl0;
-  const T kzk = (T)(kTwoPi * (double)kz);
-  Cx<T> acc[S::R2];
-#pragma unroll
-  for (int i = 0; i < S::R2; ++i) acc[i] = cx<T>(0, 0);
-  const int lane = threadIdx.x & 31;
-  const int bline = lane / S::R1;
-  const int k1 = lane - bline * S::R1;
-  for (int t = 0; t < O.nterms; ++t) {
-    const Cx<T>* sl = slab + (t * LPC + wl0) * S::L;
-    const int ax = O.axis[t];
-    auto load = [&](int line, int x, int) -> Cx<T> { return sl[line * S::L + x]; };
-    auto store = [&](int line, int q, int k2, Cx<T> v) {
-      const int ix = bin_to_index(q, S::L, K0, B0);
-      if (ix < 0) return;
-      if (ax == 0) v = mul_ik<T>(v, (T)(kTwoPi * (double)freq_of(ix, K0, B0)));
-      else if (ax == 1) v = mul_ik<T>(v, (T)(kTwoPi * (double)freq_of(ky0 + line, g.K[1], B1)));
-      else if (ax == 2) v = mul_ik<T>(v, kzk);
-      acc[k2] = cadd(acc[k2], v);
-    };
-    wfft<T, S, false>(tile, tw, nl, load, store);
-  }
-  if (bline >= nl || bline >= S::LPW) return;
-  const int ky = ky0 + bline;
-#pragma unroll
-  for (int k2 = 0; k2 < S::R2; ++k2) {
-    const int ix = bin_to_index(k1 + S::R1 * k2, S::L, K0, B0);
-    if (ix < 0) continue;
-    const Cx<T> rr = cscale(acc[k2], a.scale);
-    if (kz == 0) {
-      a.z0[(int64_t)o * B0 * B1 + ix * B1 + ky] = rr;
-    } else {
-      const int64_t e = ((int64_t)kz * B0 + ix) * B1 + ky;
-      epilogue<T>(a, O, (int64_t)o * g.nh + e, e, rr);
+  const int nitems = a.no * per;
+  auto issue = [&](int it, int t, int b) {
+    const int o = it / per;
+    const int r = it - o * per;
+    const int kz = r / nyb;
+    const int cky0 = (r - kz * nyb) * LPC;
+    const int nlc = min(LPC, B1 - cky0);
+    const Cx<T>* src = a.in + a.o[o].f[t] * g.n1 + ((int64_t)kz * B1 + cky0) * S::L;
+    Cx<T>* dst = slab + b * SLAB;
+    for (int i = threadIdx.x; i < nlc * S::L; i += blockDim.x) {
+      const int row = i / S::L;
+      cp_async<T>(dst + row * LS + (i - row * S::L), src + i);
     }
+  };
+  load_tw<T>(tw, twg, S::L);
+  int it = blockIdx.x, t = 0, b = 0;
+  if (it < nitems) issue(it, 0, 0);
+  __pipeline_commit();
+  const int wl0 = (threadIdx.x >> 5) * S::LPW;
+  while (it < nitems) {
+    const int o = it / per;
+    const FwdOut<T>& O = a.o[o];
+    const int nt = O.nterms;
+    int nit = it, ntt = t + 1;
+    if (ntt >= nt) { nit = it + gridDim.x; ntt = 0; }
+    if (nit < nitems) issue(nit, ntt, b ^ 1);
+    __pipeline_commit();
+    __pipeline_wait_prior(1);
+    __syncthreads();
+    const int r = it - o * per;
+    const int kz = r / nyb;
+    const int cky0 = (r - kz * nyb) * LPC;
+    const int nl = min(S::LPW, min(LPC, B1 - cky0) - wl0);
+    const int ky0 = cky0 + wl0;
+    if (nl > 0) {
+      const T kzk = (T)(kTwoPi * (double)kz);
+      const Cx<T>* sl = slab + b * SLAB + wl0 * LS;
+      const int ax = O.axis[t];
+      auto load = [&](int line, int x, int) -> Cx<T> { return sl[line * LS + x]; };
+      auto store = [&](int line, int q, int, Cx<T> v) {
+        const int ix = bin_to_index(q, S::L, K0, B0);
+        if (ix < 0) return;
+        if (ax == 0) v = mul_ik<T>(v, (T)(kTwoPi * (double)freq_of(ix, K0, B0)));
+        else if (ax == 1) v = mul_ik<T>(v, (T)(kTwoPi * (double)freq_of(ky0 + line, g.K[1], B1)));
+        else if (ax == 2) v = mul_ik<T>(v, kzk);
+        Cx<T>* rp = res + ix * LPCS + wl0 + line;  // owned by this lane for every term
+        *rp = t == 0 ? v : cadd(*rp, v);
+      };
+      wfft<T, S, false, true>(slab + b * SLAB + wl0 * LS, tw, nl, load, store);
+    }
+    if (t == nt - 1) {
+      __syncthreads();
+      const int nlc = min(LPC, B1 - cky0);
+      if (kz == 0) {
+        for (int i = threadIdx.x; i < B0 * nlc; i += blockDim.x) {
+          const int ix = i / nlc, l = i - (i / nlc) * nlc;
+          a.z0[(int64_t)o * B0 * B1 + ix * B1 + cky0 + l] = cscale(res[ix * LPCS + l], a.scale);
+        }
+      } else {
+        epilogue_block<T, LPCS>(a, O, o, kz, cky0, nlc, g, res);
+      }
+    }
+    __syncthreads();
+    it = nit;
+    t = ntt;
+    b ^= 1;
   }
 }
 
@@ -822,6 +991,20 @@ struct PadEngine {
 
 // raise the kernel's dynamic shared-memory limit once (not per launch)
 template <class K>
+static int persistent_grid(K kernel, int threads, size_t smem, int nitems) {
+  static int per_sm = 0;  // one static per kernel instantiation (smem is fixed per instantiation)
+  static int nsm = 0;
+  if (!per_sm) {
+    int dev;
+    BLR_CUDA(cudaGetDevice(&dev));
+    BLR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    BLR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+    if (per_sm < 1) per_sm = 1;
+  }
+  return std::max(1, std::min(nitems, per_sm * nsm));
+}
+
+template <typename K>
 static void ensure_smem(K kernel, size_t bytes) {
   static size_t set = 48 * 1024;  // one static per kernel instantiation
   if (bytes > set) {
@@ -837,7 +1020,7 @@ template <typename T, class S>
 void launch_xinv(blr_ctx* c, PadEngine* e, const XPassArgs<T>& a) {
   const PadGeom& g = e->g;
   constexpr int LPC = kPW * S::LPW;
-  const size_t sm = sizeof(Cx<T>) * (S::L + (size_t)g.B[0] * LPC + kPW * S::TILE);
+  const size_t sm = sizeof(Cx<T>) * (S::L + (size_t)g.B[0] * t_stride<LPC>() + kPW * S::TILE);
   ensure_smem(k_xinv<T, S>, sm);
   const int nyb = (g.B[1] + LPC - 1) / LPC;
   k_xinv<T, S><<<a.nx * g.Kz1 * nyb, kPW * 32, sm, c->stream>>>(a, g, e->tw[0]);
@@ -849,7 +1032,7 @@ void launch_yinv(blr_ctx* c, PadEngine* e, const YPassArgs<T>& a) {
   constexpr int LPC = kPW * S::LPW;
   int ntmax = 1;
   for (int i = 0; i < a.ny; ++i) ntmax = std::max(ntmax, a.nterms[i]);
-  const size_t sm = sizeof(Cx<T>) * (S::L + (size_t)ntmax * g.B[1] * LPC + kPW * S::TILE);
+  const size_t sm = sizeof(Cx<T>) * (S::L + (size_t)ntmax * g.B[1] * t_stride<LPC>() + kPW * S::TILE);
   ensure_smem(k_yinv<T, S>, sm);
   const int nxb = (g.P[0] + LPC - 1) / LPC;
   k_yinv<T, S><<<a.ny * g.Kz1 * nxb, kPW * 32, sm, c->stream>>>(a, g, e->tw[1], ntmax);
@@ -877,25 +1060,27 @@ void launch_lines(blr_ctx* c, PadEngine* e, const LineArgs<T>& a) {
   BLR_LAUNCHED();
 }
 template <typename T, class S>
-void launch_yfwd(blr_ctx* c, PadEngine* e, const Cx<T>* in, int nf, Cx<T>* out) {
+void launch_yfwd(blr_ctx* c, PadEngine* e, const YFwdArgs<T>& a) {
   const PadGeom& g = e->g;
   constexpr int LPC = kPW * S::LPW;
-  const size_t sm = sizeof(Cx<T>) * (S::L + (size_t)LPC * S::L + kPW * S::TILE);
+  const size_t sm = sizeof(Cx<T>) * (S::L + 2 * (size_t)LPC * row_stride<T, S, true>() +
+                                     (size_t)g.B[1] * t_stride<LPC>());
   ensure_smem(k_yfwd<T, S>, sm);
   const int nxb = (g.P[0] + LPC - 1) / LPC;
-  k_yfwd<T, S><<<nf * g.Kz1 * nxb, kPW * 32, sm, c->stream>>>(in, out, g, e->tw[1]);
+  const int grid = persistent_grid(k_yfwd<T, S>, kPW * 32, sm, a.nj * g.Kz1 * nxb);
+  k_yfwd<T, S><<<grid, kPW * 32, sm, c->stream>>>(a, g, e->tw[1]);
   BLR_LAUNCHED();
 }
 template <typename T, class S>
 void launch_xfwd(blr_ctx* c, PadEngine* e, const FwdArgs<T>& a) {
   const PadGeom& g = e->g;
   constexpr int LPC = kPW * S::LPW;
-  int ntmax = 1;
-  for (int i = 0; i < a.no; ++i) ntmax = std::max(ntmax, a.o[i].nterms);
-  const size_t sm = sizeof(Cx<T>) * (S::L + (size_t)ntmax * LPC * S::L + kPW * S::TILE);
+  const size_t sm = sizeof(Cx<T>) * (S::L + 2 * (size_t)LPC * row_stride<T, S, true>() +
+                                     (size_t)g.B[0] * t_stride<LPC>());
   ensure_smem(k_xfwd<T, S>, sm);
   const int nyb = (g.B[1] + LPC - 1) / LPC;
-  k_xfwd<T, S><<<a.no * g.Kz1 * nyb, kPW * 32, sm, c->stream>>>(a, g, e->tw[0], ntmax);
+  const int grid = persistent_grid(k_xfwd<T, S>, kPW * 32, sm, a.no * g.Kz1 * nyb);
+  k_xfwd<T, S><<<grid, kPW * 32, sm, c->stream>>>(a, g, e->tw[0]);
   BLR_LAUNCHED();
 }
 
