@@ -234,11 +234,15 @@ static void acc_tables(int op, LineArgs<T>& a) {
   }
 }
 
+static const char* const kLineOpName[] = {"pad_zlines_realize", "pad_zlines_map",     "pad_zlines_map_tc",
+                                          "pad_zlines_map_tf",  "pad_zlines_inv_vol", "pad_zlines_bwd_vol",
+                                          "pad_zlines_outer",   "pad_zlines_outer_pair", "pad_zlines_contract"};
+
 template <typename T, int OP>
 static void lines(blr_ctx* c, PadEngine* e, LineArgs<T>& a, double bytes) {
   a.op = OP;
   acc_tables<T>(OP, a);
-  ProfScope ps(c, "pad_zlines", bytes);
+  ProfScope ps(c, kLineOpName[OP], bytes);
   dispatch_lines<T, OP>(c, e, a);
 }
 

@@ -356,7 +356,9 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
   const int x = blockIdx.x / nyc;
   const int y0 = (blockIdx.x - x * nyc) * LPC + warp * S::LPW;
   const int ns_blk = OP == kOpContract ? a.d : a.ns;
-  const int nreal = (Tr::acc || OP == kOpRealize) ? 0 : ns_blk;
+  // real fields kept in shared memory: REAL ops' realized inputs; the
+  // contraction's realized rho_n (d fields, refilled per node)
+  const int nreal = OP == kOpContract ? a.d : (Tr::acc || OP == kOpRealize) ? 0 : ns_blk;
   // shared layout: tw | per warp { tile | stage[max(2*2*Kz1*LPW, LPW*L)] (xbuf aliases it after the
   //                                 C2R phase) | Vst[nst][LPW*L] | Rsm[nreal][LPW*L] }
   const int fstride = (Kz1 + 1) * S::LPW;  // per-field stage: Kz1 spectra rows + one zero row
@@ -467,9 +469,9 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
         break;
       }
       const Cx<T>* src = a.sin[f] + noff + sline;
-      for (int i = lane; i < Kz1 * nl; i += 32) {
-        const int k = i / nl, l = i - (i / nl) * nl;
-        __pipeline_memcpy_async(st + ff * fstride + k * S::LPW + l, src + k * kzs + l, sizeof(Cx<T>));
+      for (int i = lane; i < Kz1 * S::LPW; i += 32) {
+        const int k = i / S::LPW, l = i - (i / S::LPW) * S::LPW;  // compile-time divisor
+        if (l < nl) __pipeline_memcpy_async(st + ff * fstride + i, src + k * kzs + l, sizeof(Cx<T>));
       }
     }
     __pipeline_commit();
@@ -514,21 +516,9 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
       if constexpr (OP == kOpRealize) {
         a.wout[f][gi] = v.x;
         if (two) a.wout[f + 1][gi] = v.y;
-      } else if constexpr (!Tr::acc) {
+      } else if constexpr (!Tr::acc || OP == kOpContract) {
         Rsm[f * ldR + li] = v.x;
         if (two) Rsm[(f + 1) * ldR + li] = v.y;
-      } else if constexpr (OP == kOpContract) {
-        const T wn = (T)a.w[node];
-        const int64_t go = gi + node * a.rin_node_stride;
-#pragma unroll
-        for (int o = 0; o < NOM; ++o) {
-          if (o < a.d) {
-            const T m1 = __ldg(a.rin[a.mi[o][f]] + go);
-            T c = m1 * v.x;
-            if (two) c += __ldg(a.rin[a.mi[o][f + 1]] + go) * v.y;
-            acc[o][k2] += wn * c;
-          }
-        }
       } else {
         if (OP == kOpMap && a.wout[f]) {
           a.wout[f][gi] = v.x;
@@ -539,6 +529,49 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
       }
     };
     wfft<T, S, true>(tile, tw, nl, load, store);
+    if constexpr (OP == kOpContract) {
+      if (p == npair - 1) {
+        // node complete: rho_n is realized in Rsm.  Stream the cached D(phi_n)
+        // fields with lane-contiguous (coalesced) loads, two positions x d^2
+        // fields issued per batch; lane owns positions li = lane + 32 m.
+        __syncwarp();
+        const int d = a.d;
+        const T wn = (T)a.w[node];
+        const T* Mb[3][3];
+#pragma unroll
+        for (int o = 0; o < 3; ++o)
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            Mb[o][j] = a.rin[(o < d && j < d) ? a.mi[o][j] : 0] + rline + node * a.rin_node_stride;
+        const int npos = nl * L;
+#pragma unroll
+        for (int m0 = 0; m0 < S::R2; m0 += 2) {
+          T mv[2][3][3];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int li = lane + 32 * (m0 + u);
+            const bool ok = m0 + u < S::R2 && li < npos;
+#pragma unroll
+            for (int o = 0; o < 3; ++o)
+#pragma unroll
+              for (int j = 0; j < 3; ++j) mv[u][o][j] = (ok && o < d && j < d) ? __ldg(Mb[o][j] + li) : (T)0;
+          }
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int li = lane + 32 * (m0 + u);
+            if (m0 + u < S::R2 && li < npos) {
+              T r[3];
+#pragma unroll
+              for (int j = 0; j < 3; ++j) r[j] = j < d ? Rsm[j * ldR + li] : (T)0;
+#pragma unroll
+              for (int o = 0; o < NOM; ++o)
+                acc[o][m0 + u] += wn * (mv[u][o][0] * r[0] + mv[u][o][1] * r[1] + mv[u][o][2] * r[2]);
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
     if constexpr (Tr::acc && OP != kOpContract) {
       // uniform (per pair) output selection, then unrolled accumulation
       if (own) {
@@ -569,7 +602,20 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
   const int no = a.no;
   for (int o = 0; o < no; o += 2) {
     const bool two = o + 1 < no;
-    if constexpr (Tr::acc) {
+    if constexpr (OP == kOpContract) {
+#pragma unroll
+      for (int m = 0; m < S::R2; ++m) {
+        const int li = lane + 32 * m;
+        T v1 = 0, v2 = 0;
+#pragma unroll
+        for (int q = 0; q < NOM; ++q) {
+          if (q == o) v1 = acc[q][m];
+          if (q == o + 1) v2 = acc[q][m];
+        }
+        if (li < nl * L) xbuf[li] = cx<T>(v1, v2);
+      }
+      __syncwarp();
+    } else if constexpr (Tr::acc) {
       if (own) {
 #pragma unroll
         for (int k2 = 0; k2 < S::R2; ++k2) {
@@ -584,20 +630,19 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
       }
       __syncwarp();
     }
+    // Outer: output o = (i, j) pairs, index math hoisted out of the gather
+    const int oi1 = o / a.d, oj1 = o - oi1 * a.d;
+    const int oi2 = two ? (o + 1) / a.d : 0, oj2 = two ? o + 1 - oi2 * a.d : 0;
+    const T* R1p = Rsm + oi1 * ldR;
+    const T* R2p = Rsm + oi2 * ldR;
     auto load = [&](int line, int z, int n1) -> Cx<T> {
       if constexpr (Tr::acc) {
         return xbuf[line * L + z];
       } else if constexpr (OP == kOpOuter) {
-        const int d = a.d, li = line * L + z;
-        const int i1 = o / d, j1 = o - i1 * d;
-        const T v1 = j1 == 0 ? vreg[0][n1] : (j1 == 1 ? vreg[1][n1] : vreg[2][n1]);
-        T r2 = 0;
-        if (two) {
-          const int i2 = (o + 1) / d, j2 = o + 1 - i2 * d;
-          const T v2 = j2 == 0 ? vreg[0][n1] : (j2 == 1 ? vreg[1][n1] : vreg[2][n1]);
-          r2 = Rsm[i2 * ldR + li] * v2;
-        }
-        return cx<T>(Rsm[i1 * ldR + li] * v1, r2);
+        const int li = line * L + z;
+        const T v1 = oj1 == 0 ? vreg[0][n1] : (oj1 == 1 ? vreg[1][n1] : vreg[2][n1]);
+        const T v2 = oj2 == 0 ? vreg[0][n1] : (oj2 == 1 ? vreg[1][n1] : vreg[2][n1]);
+        return cx<T>(R1p[li] * v1, two ? R2p[li] * v2 : (T)0);
       } else {
         const int li = line * L + z;
         const int64_t gi = rline + li;
@@ -609,8 +654,9 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
     wfft<T, S, false>(tile, tw, nl, load, store);
     Cx<T>* O1 = a.sout[o] + sline;
     Cx<T>* O2 = two ? a.sout[o + 1] + sline : nullptr;
-    for (int idx = lane; idx < nl * Kz1; idx += 32) {
-      const int k = idx / nl, l = idx - (idx / nl) * nl;
+    for (int idx = lane; idx < S::LPW * Kz1; idx += 32) {
+      const int k = idx / S::LPW, l = idx - (idx / S::LPW) * S::LPW;  // compile-time divisor
+      if (l >= nl) continue;
       const Cx<T> Z = xbuf[l * L + k];
       Cx<T> Zm = xbuf[l * L + (k == 0 ? 0 : L - k)];
       Zm.y = -Zm.y;
@@ -704,9 +750,9 @@ __global__ void __launch_bounds__(kPW * 32, 4) k_yfwd(YFwdArgs<T> a, PadGeom g, 
       __syncthreads();
       const int nlc = min(LPC, P0 - cx0);
       Cx<T>* dst = a.out + jb * g.n1 + (int64_t)kz * B1 * P0 + cx0;
-      for (int i = threadIdx.x; i < B1 * nlc; i += blockDim.x) {
-        const int iy = i / nlc, l = i - (i / nlc) * nlc;
-        dst[iy * P0 + l] = res[iy * LPCS + l];
+      for (int i = threadIdx.x; i < B1 * LPC; i += blockDim.x) {
+        const int iy = i / LPC, l = i - (i / LPC) * LPC;  // compile-time divisor
+        if (l < nlc) dst[iy * P0 + l] = res[iy * LPCS + l];
       }
     }
     __syncthreads();
@@ -783,12 +829,12 @@ __device__ __forceinline__ void epilogue(const FwdArgs<T>& a, const FwdOut<T>& O
 // tile res[ix][LPCS]: consecutive threads take consecutive ky (coalesced), and
 // each thread issues the operand loads of U elements before any store, so the
 // RK4 read-modify-write costs one memory latency per U elements, not one each.
-template <typename T, int LPCS>
+template <typename T, int LPC, int LPCS>
 __device__ __forceinline__ void epilogue_block(const FwdArgs<T>& a, const FwdOut<T>& O, int o, int kz,
                                                int cky0, int nlc, const PadGeom& g, const Cx<T>* res) {
   constexpr int U = 2;
   const int B0 = g.B[0], B1 = g.B[1];
-  const int n = B0 * nlc;
+  const int n = B0 * LPC;
   const int s = a.rk_s;
   for (int i0 = threadIdx.x; i0 < n; i0 += U * blockDim.x) {
     Cx<T> r[U], v[U], cc[U], ac[U];
@@ -796,8 +842,8 @@ __device__ __forceinline__ void epilogue_block(const FwdArgs<T>& a, const FwdOut
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = i0 + u * blockDim.x;
-      if (i >= n) continue;
-      const int ix = i / nlc, l = i - (i / nlc) * nlc;
+      const int ix = i / LPC, l = i - (i / LPC) * LPC;  // compile-time divisor
+      if (i >= n || l >= nlc) continue;
       e[u] = ((int64_t)kz * B0 + ix) * B1 + cky0 + l;
       r[u] = cscale(res[ix * LPCS + l], a.scale);
       const int64_t h = (int64_t)o * g.nh + e[u];
@@ -808,7 +854,7 @@ __device__ __forceinline__ void epilogue_block(const FwdArgs<T>& a, const FwdOut
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = i0 + u * blockDim.x;
-      if (i >= n) continue;
+      if (i >= n || i - (i / LPC) * LPC >= nlc) continue;
       const int64_t h = (int64_t)o * g.nh + e[u];
       Cx<T> k;
       if (O.mode == kEpiNegAdd) k = cx<T>(-(v[u].x + r[u].x), -(v[u].y + r[u].y));
@@ -901,12 +947,12 @@ __global__ void __launch_bounds__(kPW * 32, 3) k_xfwd(FwdArgs<T> a, PadGeom g, c
       __syncthreads();
       const int nlc = min(LPC, B1 - cky0);
       if (kz == 0) {
-        for (int i = threadIdx.x; i < B0 * nlc; i += blockDim.x) {
-          const int ix = i / nlc, l = i - (i / nlc) * nlc;
-          a.z0[(int64_t)o * B0 * B1 + ix * B1 + cky0 + l] = cscale(res[ix * LPCS + l], a.scale);
+        for (int i = threadIdx.x; i < B0 * LPC; i += blockDim.x) {
+          const int ix = i / LPC, l = i - (i / LPC) * LPC;
+          if (l < nlc) a.z0[(int64_t)o * B0 * B1 + ix * B1 + cky0 + l] = cscale(res[ix * LPCS + l], a.scale);
         }
       } else {
-        epilogue_block<T, LPCS>(a, O, o, kz, cky0, nlc, g, res);
+        epilogue_block<T, LPC, LPCS>(a, O, o, kz, cky0, nlc, g, res);
       }
     }
     __syncthreads();
@@ -1042,7 +1088,7 @@ template <typename T, class S, int OP>
 void launch_lines(blr_ctx* c, PadEngine* e, const LineArgs<T>& a) {
   const PadGeom& g = e->g;
   const int ns_blk = OP == kOpContract ? a.d : a.ns;
-  const int nreal = (ZOp<OP>::acc || OP == kOpRealize) ? 0 : ns_blk;
+  const int nreal = OP == kOpContract ? a.d : (ZOp<OP>::acc || OP == kOpRealize) ? 0 : ns_blk;
   const int nst = ZOp<OP>::acc ? a.nst : 0;
   const size_t stage_n = std::max<size_t>(4 * (size_t)(g.Kz1 + 1) * S::LPW, (size_t)S::LPW * S::L);
   const size_t warp_bytes = sizeof(Cx<T>) * ((size_t)S::TILE + stage_n) +
