@@ -402,37 +402,6 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
   for (int o = 0; o < NOM; ++o)
 #pragma unroll
     for (int k2 = 0; k2 < S::R2; ++k2) acc[o][k2] = 0;
-  if constexpr (OP == kOpMapTC) {
-    // acc_i = sum_j Du_ij dV_j  (rin: Du [0,dd) V [dd,dd+d) dV [dd+d, dd+2d)); branch-free
-    // unrolled loads (absent components read component 0 and are masked)
-    if (own) {
-      const int d = a.d, dd = d * d;
-      const T* du[3][3];
-      const T* dv[3];
-      T msk[3];
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        const int jc = j < d ? j : 0;
-        msk[j] = j < d ? (T)1 : (T)0;
-        dv[j] = a.rin[dd + d + jc] + rline + bl * L + k1;
-#pragma unroll
-        for (int o = 0; o < 3; ++o) du[o][j] = a.rin[(o < d ? o : 0) * d + jc] + rline + bl * L + k1;
-      }
-#pragma unroll
-      for (int k2 = 0; k2 < S::R2; ++k2) {
-        T vj[3];
-#pragma unroll
-        for (int j = 0; j < 3; ++j) vj[j] = msk[j] * __ldg(dv[j] + S::R1 * k2);
-#pragma unroll
-        for (int o = 0; o < NOM; ++o) {
-          T s = 0;
-#pragma unroll
-          for (int j = 0; j < 3; ++j) s += __ldg(du[o < 3 ? o : 0][j] + S::R1 * k2) * vj[j];
-          acc[o][k2] = s;
-        }
-      }
-    }
-  }
   // per-lane Hermitian gather table for step A (lane n2, rows k = R2*n1 + n2):
   // stage row index and sign s: G = (F1.x - s F2.y, s F1.y + F2.x)
   int hidx[S::R1], hsg[S::R1];
@@ -476,7 +445,7 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
     }
     __pipeline_commit();
   };
-  T sv1[S::R2], sv2[S::R2];
+  prefetch(0);  // first spectra in flight while the per-lane register operands load
   // Outer: V_j at this lane's step-A positions (line la, z = R2*n1 + n2), used by every R2C gather
   T vreg[OP == kOpOuter ? 3 : 1][OP == kOpOuter ? S::R1 : 1];
   if constexpr (OP == kOpOuter) {
@@ -489,7 +458,37 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
       for (int n1 = 0; n1 < S::R1; ++n1) vreg[j][n1] = oka ? __ldg(vj + S::R2 * n1) : (T)0;
     }
   }
-  prefetch(0);
+  if constexpr (OP == kOpMapTC) {
+    // acc_i = sum_j Du_ij dV_j  (rin: Du [0,dd) V [dd,dd+d) dV [dd+d, dd+2d)); branch-free
+    // unrolled loads (absent components read component 0 and are masked)
+    if (own) {
+      const int d = a.d, dd = d * d;
+      const T* du[3][3];
+      const T* dv[3];
+      T msk[3];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int jc = j < d ? j : 0;
+        msk[j] = j < d ? (T)1 : (T)0;
+        dv[j] = a.rin[dd + d + jc] + rline + bl * L + k1;
+#pragma unroll
+        for (int o = 0; o < 3; ++o) du[o][j] = a.rin[(o < d ? o : 0) * d + jc] + rline + bl * L + k1;
+      }
+#pragma unroll
+      for (int k2 = 0; k2 < S::R2; ++k2) {
+        T vj[3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) vj[j] = msk[j] * __ldg(dv[j] + S::R1 * k2);
+#pragma unroll
+        for (int o = 0; o < NOM; ++o) {
+          T s = 0;
+#pragma unroll
+          for (int j = 0; j < 3; ++j) s += __ldg(du[o < 3 ? o : 0][j] + S::R1 * k2) * vj[j];
+          acc[o][k2] = s;
+        }
+      }
+    }
+  }
   for (int q = 0; q < total; ++q) {
     if (q + 1 < total) {
       prefetch(q + 1);
@@ -503,6 +502,21 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
     const bool two = f + 1 < ns_blk;
     const Cx<T>* st1 = stage + (q & 1) * 2 * fstride;
     const Cx<T>* st2 = st1 + fstride;
+    // ACC ops: per-pair output coefficients (uniform), applied in the FFT store
+    T c1[NOM], c2[NOM];
+    const T* V1 = Vst;
+    const T* V2 = Vst;
+    if constexpr (Tr::acc && OP != kOpContract) {
+      const int o1 = a.oi[f], o2 = two ? a.oi[f + 1] : -1;
+      const T sg1 = (T)a.sg[f], sg2 = two ? (T)a.sg[f + 1] : (T)0;
+#pragma unroll
+      for (int o = 0; o < NOM; ++o) {
+        c1[o] = o == o1 ? sg1 : (T)0;
+        c2[o] = o == o2 ? sg2 : (T)0;
+      }
+      V1 = Vst + a.ri[f] * ldR;
+      V2 = Vst + (two ? a.ri[f + 1] : 0) * ldR;
+    }
     auto load = [&](int line, int, int n1) -> Cx<T> {
       // branch-free Hermitian packing of F1 + i F2 (zero rows index the zero pad row)
       const Cx<T> F1 = st1[hidx[n1] + line];
@@ -524,8 +538,10 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
           a.wout[f][gi] = v.x;
           if (two) a.wout[f + 1][gi] = v.y;
         }
-        sv1[k2] = v.x;
-        sv2[k2] = v.y;
+        const T p1 = v.x * V1[li];
+        const T p2 = v.y * V2[li];
+#pragma unroll
+        for (int o = 0; o < NOM; ++o) acc[o][k2] += c1[o] * p1 + c2[o] * p2;
       }
     };
     wfft<T, S, true>(tile, tw, nl, load, store);
@@ -570,31 +586,6 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
           }
         }
         __syncwarp();
-      }
-    }
-    if constexpr (Tr::acc && OP != kOpContract) {
-      // uniform (per pair) output selection, then unrolled accumulation
-      if (own) {
-        const int o1 = a.oi[f], r1 = a.ri[f];
-        const T sg1 = (T)a.sg[f];
-        const T* V1 = Vst + r1 * ldR + bl * L + k1;
-#pragma unroll
-        for (int o = 0; o < NOM; ++o)
-          if (o == o1) {
-#pragma unroll
-            for (int k2 = 0; k2 < S::R2; ++k2) acc[o][k2] += sg1 * sv1[k2] * V1[S::R1 * k2];
-          }
-        if (two) {
-          const int o2 = a.oi[f + 1], r2 = a.ri[f + 1];
-          const T sg2 = (T)a.sg[f + 1];
-          const T* V2 = Vst + r2 * ldR + bl * L + k1;
-#pragma unroll
-          for (int o = 0; o < NOM; ++o)
-            if (o == o2) {
-#pragma unroll
-              for (int k2 = 0; k2 < S::R2; ++k2) acc[o][k2] += sg2 * sv2[k2] * V2[S::R1 * k2];
-            }
-        }
       }
     }
   }
