@@ -78,6 +78,87 @@ __device__ __forceinline__ void cp_async(Cx<T>* dst, const Cx<T>* src) {
   __pipeline_memcpy_async(dst, src, sizeof(Cx<T>));
 }
 
+// --- bulk-copy (TMA engine) staging --------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Double-buffered slab staging for the persistent pass kernels.  fp64 rows are
+// whole 16-byte multiples: warp 0 arms the buffer's mbarrier with the byte
+// count and issues one cp.async.bulk per row (the copy engine writes the
+// padded smem rows; no per-element instructions); every thread then waits on
+// the mbarrier parity.  fp32 rows may be 8-byte aligned only: per-element
+// cp.async with commit / wait_group and a CTA barrier.
+template <typename T>
+struct Stager {
+  static constexpr bool kBulk = sizeof(T) == 8;
+  uint64_t* bar;  // [2] in shared memory
+  uint32_t phase;
+  __device__ __forceinline__ void init(uint64_t* b) {
+    bar = b;
+    phase = 0;
+    if (kBulk && threadIdx.x == 0) {
+      mbar_init(bar, 1);
+      mbar_init(bar + 1, 1);
+      fence_mbar_init();
+    }
+  }
+  // start a load into buffer b of `bytes` in total (bulk: arm the mbarrier
+  // before warp 0 issues any copy of it)
+  __device__ __forceinline__ void begin(int b, uint32_t bytes) {
+    if constexpr (kBulk) {
+      if (threadIdx.x < 32) {
+        if (threadIdx.x == 0) mbar_expect_tx(bar + b, bytes);
+        __syncwarp();
+      }
+    }
+  }
+  // nrows rows of ncols elements: global row stride gs, shared row stride ss
+  __device__ __forceinline__ void rows(Cx<T>* dst, int ss, const Cx<T>* src, int64_t gs, int nrows, int ncols, int b) {
+    if constexpr (kBulk) {
+      if (threadIdx.x < 32)
+        for (int r = threadIdx.x; r < nrows; r += 32)
+          bulk_g2s(dst + r * ss, src + r * gs, (uint32_t)(ncols * sizeof(Cx<T>)), bar + b);
+    } else {
+      for (int i = threadIdx.x; i < nrows * ncols; i += blockDim.x) {
+        const int r = i / ncols, c = i - (i / ncols) * ncols;
+        cp_async<T>(dst + r * ss + c, src + r * gs + c);
+      }
+    }
+  }
+  __device__ __forceinline__ void commit() {
+    if constexpr (!kBulk) __pipeline_commit();
+  }
+  // wait for buffer b (the other buffer's load may stay in flight)
+  __device__ __forceinline__ void wait(int b) {
+    if constexpr (kBulk) {
+      mbar_wait(bar + b, (phase >> b) & 1u);
+      phase ^= 1u << b;
+    } else {
+      __pipeline_wait_prior(1);
+      __syncthreads();
+    }
+  }
+};
+
 // Staged pass kernels: kPW warps per CTA; the CTA's whole input slab is
 // copied to shared memory with coalesced cp.async first, then every warp runs
 // its four-step FFTs from shared memory.
@@ -691,6 +772,10 @@ __global__ void __launch_bounds__(kPW * 32, 4) k_yfwd(YFwdArgs<T> a, PadGeom g, 
   const int nxb = (P0 + LPC - 1) / LPC;
   const int per = g.Kz1 * nxb;
   const int nitems = a.nj * per;
+  __shared__ uint64_t bars[2];
+  Stager<T> stg;
+  stg.init(bars);
+  __syncthreads();
   auto issue = [&](int it, int t, int b) {
     const int jb = it / per;
     const int r = it - jb * per;
@@ -698,26 +783,23 @@ __global__ void __launch_bounds__(kPW * 32, 4) k_yfwd(YFwdArgs<T> a, PadGeom g, 
     const int cx0 = (r - kz * nxb) * LPC;
     const int nlc = min(LPC, P0 - cx0);
     const Cx<T>* src = a.sin[jb][t] + ((int64_t)kz * P0 + cx0) * S::L;  // nlc contiguous rows
-    Cx<T>* dst = slab + b * SLAB;
-    for (int i = threadIdx.x; i < nlc * S::L; i += blockDim.x) {
-      const int row = i / S::L;
-      cp_async<T>(dst + row * LS + (i - row * S::L), src + i);
-    }
+    stg.begin(b, (uint32_t)(nlc * S::L * sizeof(Cx<T>)));
+    stg.rows(slab + b * SLAB, LS, src, S::L, nlc, S::L, b);
   };
   load_tw<T>(tw, twg, S::L);
   int it = blockIdx.x, t = 0, b = 0;
   if (it < nitems) issue(it, 0, 0);
-  __pipeline_commit();
+  stg.commit();
   const int wl0 = (threadIdx.x >> 5) * S::LPW;
+  __syncthreads();  // twiddles
   while (it < nitems) {
     const int jb = it / per;
     const int nt = a.nterms[jb];
     int nit = it, ntt = t + 1;
     if (ntt >= nt) { nit = it + gridDim.x; ntt = 0; }
     if (nit < nitems) issue(nit, ntt, b ^ 1);
-    __pipeline_commit();
-    __pipeline_wait_prior(1);
-    __syncthreads();
+    stg.commit();
+    stg.wait(b);
     const int r = it - jb * per;
     const int kz = r / nxb;
     const int cx0 = (r - kz * nxb) * LPC;
@@ -738,9 +820,9 @@ __global__ void __launch_bounds__(kPW * 32, 4) k_yfwd(YFwdArgs<T> a, PadGeom g, 
       wfft<T, S, false, true>(slab + b * SLAB + wl0 * LS, tw, nl, load, store);
     }
     if (t == nt - 1) {
-      __syncthreads();
       const int nlc = min(LPC, P0 - cx0);
       Cx<T>* dst = a.out + jb * g.n1 + (int64_t)kz * B1 * P0 + cx0;
+      __syncthreads();
       for (int i = threadIdx.x; i < B1 * LPC; i += blockDim.x) {
         const int iy = i / LPC, l = i - (i / LPC) * LPC;  // compile-time divisor
         if (l < nlc) dst[iy * P0 + l] = res[iy * LPCS + l];
@@ -885,6 +967,10 @@ __global__ void __launch_bounds__(kPW * 32, 3) k_xfwd(FwdArgs<T> a, PadGeom g, c
   const int nyb = (B1 + LPC - 1) / LPC;
   const int per = g.Kz1 * nyb;
   const int nitems = a.no * per;
+  __shared__ uint64_t bars[2];
+  Stager<T> stg;
+  stg.init(bars);
+  __syncthreads();
   auto issue = [&](int it, int t, int b) {
     const int o = it / per;
     const int r = it - o * per;
@@ -892,17 +978,15 @@ __global__ void __launch_bounds__(kPW * 32, 3) k_xfwd(FwdArgs<T> a, PadGeom g, c
     const int cky0 = (r - kz * nyb) * LPC;
     const int nlc = min(LPC, B1 - cky0);
     const Cx<T>* src = a.in + a.o[o].f[t] * g.n1 + ((int64_t)kz * B1 + cky0) * S::L;
-    Cx<T>* dst = slab + b * SLAB;
-    for (int i = threadIdx.x; i < nlc * S::L; i += blockDim.x) {
-      const int row = i / S::L;
-      cp_async<T>(dst + row * LS + (i - row * S::L), src + i);
-    }
+    stg.begin(b, (uint32_t)(nlc * S::L * sizeof(Cx<T>)));
+    stg.rows(slab + b * SLAB, LS, src, S::L, nlc, S::L, b);
   };
   load_tw<T>(tw, twg, S::L);
   int it = blockIdx.x, t = 0, b = 0;
   if (it < nitems) issue(it, 0, 0);
-  __pipeline_commit();
+  stg.commit();
   const int wl0 = (threadIdx.x >> 5) * S::LPW;
+  __syncthreads();  // twiddles
   while (it < nitems) {
     const int o = it / per;
     const FwdOut<T>& O = a.o[o];
@@ -910,9 +994,8 @@ __global__ void __launch_bounds__(kPW * 32, 3) k_xfwd(FwdArgs<T> a, PadGeom g, c
     int nit = it, ntt = t + 1;
     if (ntt >= nt) { nit = it + gridDim.x; ntt = 0; }
     if (nit < nitems) issue(nit, ntt, b ^ 1);
-    __pipeline_commit();
-    __pipeline_wait_prior(1);
-    __syncthreads();
+    stg.commit();
+    stg.wait(b);
     const int r = it - o * per;
     const int kz = r / nyb;
     const int cky0 = (r - kz * nyb) * LPC;
@@ -1048,6 +1131,9 @@ static void ensure_smem(K kernel, size_t bytes) {
     int dev, maxsm;
     BLR_CUDA(cudaGetDevice(&dev));
     BLR_CUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa;
+    BLR_CUDA(cudaFuncGetAttributes(&fa, kernel));
+    maxsm -= (int)fa.sharedSizeBytes;  // static shared memory (mbarriers) counts against the opt-in limit
     BLR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
     set = (size_t)maxsm;
   }
