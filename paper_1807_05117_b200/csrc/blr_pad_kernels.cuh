@@ -162,7 +162,8 @@ struct Stager {
 // Staged pass kernels: kPW warps per CTA; the CTA's whole input slab is
 // copied to shared memory with coalesced cp.async first, then every warp runs
 // its four-step FFTs from shared memory.
-constexpr int kPW = 4;
+constexpr int kPW = 4;   // inverse passes (x, y)
+constexpr int kPWF = 2;  // forward passes (y, x): measured best at 2 warps per CTA
 
 // Shared-memory strides chosen so the FFT access patterns are free of bank
 // conflicts.  Transposed tiles [row][LPC] are read by lanes walking rows, so
@@ -759,9 +760,9 @@ struct YFwdArgs {
 // the cp.async slab of the next (item, term) load streams in while the warps
 // transform the current one, so HBM stays busy through the FFT phase.
 template <typename T, class S>
-__global__ void __launch_bounds__(kPW * 32, 4) k_yfwd(YFwdArgs<T> a, PadGeom g, const double2* __restrict__ twg) {
+__global__ void __launch_bounds__(kPWF * 32, 4) k_yfwd(YFwdArgs<T> a, PadGeom g, const double2* __restrict__ twg) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int LPC = kPW * S::LPW;
+  constexpr int LPC = kPWF * S::LPW;
   constexpr int LS = row_stride<T, S, true>();
   constexpr int LPCS = t_stride<LPC>();
   constexpr int SLAB = LPC * LS;
@@ -954,9 +955,9 @@ __device__ __forceinline__ void epilogue_block(const FwdArgs<T>& a, const FwdOut
 }
 
 template <typename T, class S>
-__global__ void __launch_bounds__(kPW * 32, 3) k_xfwd(FwdArgs<T> a, PadGeom g, const double2* __restrict__ twg) {
+__global__ void __launch_bounds__(kPWF * 32, 3) k_xfwd(FwdArgs<T> a, PadGeom g, const double2* __restrict__ twg) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int LPC = kPW * S::LPW;
+  constexpr int LPC = kPWF * S::LPW;
   constexpr int LS = row_stride<T, S, true>();
   constexpr int LPCS = t_stride<LPC>();
   constexpr int SLAB = LPC * LS;
@@ -1185,25 +1186,25 @@ void launch_lines(blr_ctx* c, PadEngine* e, const LineArgs<T>& a) {
 template <typename T, class S>
 void launch_yfwd(blr_ctx* c, PadEngine* e, const YFwdArgs<T>& a) {
   const PadGeom& g = e->g;
-  constexpr int LPC = kPW * S::LPW;
+  constexpr int LPC = kPWF * S::LPW;
   const size_t sm = sizeof(Cx<T>) * (S::L + 2 * (size_t)LPC * row_stride<T, S, true>() +
                                      (size_t)g.B[1] * t_stride<LPC>());
   ensure_smem(k_yfwd<T, S>, sm);
   const int nxb = (g.P[0] + LPC - 1) / LPC;
-  const int grid = persistent_grid(k_yfwd<T, S>, kPW * 32, sm, a.nj * g.Kz1 * nxb);
-  k_yfwd<T, S><<<grid, kPW * 32, sm, c->stream>>>(a, g, e->tw[1]);
+  const int grid = persistent_grid(k_yfwd<T, S>, kPWF * 32, sm, a.nj * g.Kz1 * nxb);
+  k_yfwd<T, S><<<grid, kPWF * 32, sm, c->stream>>>(a, g, e->tw[1]);
   BLR_LAUNCHED();
 }
 template <typename T, class S>
 void launch_xfwd(blr_ctx* c, PadEngine* e, const FwdArgs<T>& a) {
   const PadGeom& g = e->g;
-  constexpr int LPC = kPW * S::LPW;
+  constexpr int LPC = kPWF * S::LPW;
   const size_t sm = sizeof(Cx<T>) * (S::L + 2 * (size_t)LPC * row_stride<T, S, true>() +
                                      (size_t)g.B[0] * t_stride<LPC>());
   ensure_smem(k_xfwd<T, S>, sm);
   const int nyb = (g.B[1] + LPC - 1) / LPC;
-  const int grid = persistent_grid(k_xfwd<T, S>, kPW * 32, sm, a.no * g.Kz1 * nyb);
-  k_xfwd<T, S><<<grid, kPW * 32, sm, c->stream>>>(a, g, e->tw[0]);
+  const int grid = persistent_grid(k_xfwd<T, S>, kPWF * 32, sm, a.no * g.Kz1 * nyb);
+  k_xfwd<T, S><<<grid, kPWF * 32, sm, c->stream>>>(a, g, e->tw[0]);
   BLR_LAUNCHED();
 }
 
