@@ -358,20 +358,20 @@ static void fwd2d(blr_ctx* c, PadEngine* e, const std::vector<FwdSpec<T>>& outs,
       dispatch_xfwd<T>(c, e, a);
     }
     const int64_t n0 = (int64_t)a.no * g.B[0] * g.B[1];
-    k_fix0<T><<<grid_blocks(n0, 256), 256, 0, c->stream>>>(a, g);
+    launch_pdl(k_fix0<T>, grid_blocks(n0, 256), 256, 0, c->stream, a, g);
     BLR_LAUNCHED();
   }
 }
 
 template <typename T>
 static void full_to_h(blr_ctx* c, PadEngine* e, const Cx<T>* full, int ncomp, Cx<T>* H) {
-  k_full_to_h<T><<<grid_blocks(e->g.nh * ncomp, 256), 256, 0, c->stream>>>(full, ncomp, e->g, H);
+  launch_pdl(k_full_to_h<T>, grid_blocks(e->g.nh * ncomp, 256), 256, 0, c->stream, full, ncomp, e->g, H);
   BLR_LAUNCHED();
 }
 
 template <typename T>
 static void h_to_full(blr_ctx* c, PadEngine* e, const Cx<T>* H, int ncomp, Cx<T>* full) {
-  k_h_to_full<T><<<grid_blocks(c->g.nb() * ncomp, 256), 256, 0, c->stream>>>(H, ncomp, e->g, full);
+  launch_pdl(k_h_to_full<T>, grid_blocks(c->g.nb() * ncomp, 256), 256, 0, c->stream, H, ncomp, e->g, full);
   BLR_LAUNCHED();
 }
 

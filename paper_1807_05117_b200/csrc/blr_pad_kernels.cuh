@@ -27,6 +27,7 @@
 #include <cmath>
 #include <array>
 #include <cstring>
+#include <utility>
 
 namespace blr {
 
@@ -76,6 +77,32 @@ struct XPassArgs {
 template <typename T>
 __device__ __forceinline__ void cp_async(Cx<T>* dst, const Cx<T>* src) {
   __pipeline_memcpy_async(dst, src, sizeof(Cx<T>));
+}
+
+// --- programmatic dependent launch ------------------------------------------
+// Every engine kernel is launched with programmatic stream serialization and
+// executes griddepcontrol.wait -- predecessor complete, its memory visible --
+// before the first access to dependent global data; constant tables, barriers
+// and index set-up run before it.  No kernel triggers early
+// (launch_dependents at entry was measured slower: waiting CTAs of the next
+// kernel then hold SM resources through the predecessor's tail); the implicit
+// trigger at grid exit still removes the launch gap between kernels
+// (-1.1 ms per deformation GN HVP, the same as replaying a CUDA graph).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  BLR_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 
 // --- bulk-copy (TMA engine) staging --------------------------------------
@@ -221,6 +248,7 @@ __global__ void __launch_bounds__(kPW * 32) k_xinv(XPassArgs<T> a, PadGeom g, co
   const int cky0 = (r - kz * nyb) * LPC;
   const int nlc = min(LPC, B1 - cky0);
   const Cx<T>* src = a.src[xf] + ((int64_t)kz * B0) * B1 + cky0;
+  pdl_wait();
   for (int i = threadIdx.x; i < B0 * LPC; i += blockDim.x) {
     const int ix = i / LPC, l = i - ix * LPC;
     if (l < nlc) cp_async<T>(slab + ix * LPCS + l, src + ix * B1 + l);
@@ -276,6 +304,7 @@ __global__ void __launch_bounds__(kPW * 32) k_yinv(YPassArgs<T> a, PadGeom g, co
   const int cx0 = (r - kz * nxb) * LPC;
   const int nlc = min(LPC, P0 - cx0);
   const int nt = a.nterms[yf];
+  pdl_wait();
   for (int t = 0; t < nt; ++t) {
     const Cx<T>* src = a.in + a.xf[yf][t] * g.n1 + (int64_t)kz * B1 * P0 + cx0;
     Cx<T>* dst = slab + t * B1 * LPCS;
@@ -458,6 +487,7 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
   const int ldR = S::LPW * L;
   load_tw<T>(tw, twz_g, L);
   __syncthreads();
+  pdl_wait();
   const int nl = min(S::LPW, P1 - y0);
   if (nl <= 0) return;
   const int64_t sline = (int64_t)x * P1 + y0;
@@ -789,6 +819,7 @@ __global__ void __launch_bounds__(kPWF * 32, 4) k_yfwd(YFwdArgs<T> a, PadGeom g,
   };
   load_tw<T>(tw, twg, S::L);
   int it = blockIdx.x, t = 0, b = 0;
+  pdl_wait();
   if (it < nitems) issue(it, 0, 0);
   stg.commit();
   const int wl0 = (threadIdx.x >> 5) * S::LPW;
@@ -984,6 +1015,7 @@ __global__ void __launch_bounds__(kPWF * 32, 3) k_xfwd(FwdArgs<T> a, PadGeom g, 
   };
   load_tw<T>(tw, twg, S::L);
   int it = blockIdx.x, t = 0, b = 0;
+  pdl_wait();
   if (it < nitems) issue(it, 0, 0);
   stg.commit();
   const int wl0 = (threadIdx.x >> 5) * S::LPW;
@@ -1040,6 +1072,7 @@ __global__ void __launch_bounds__(kPWF * 32, 3) k_xfwd(FwdArgs<T> a, PadGeom g, 
 // kz = 0 plane: symmetrize pairs (k, -k), then the same epilogue
 template <typename T>
 __global__ void k_fix0(FwdArgs<T> a, PadGeom g) {
+  pdl_wait();
   const int B0 = g.B[0], B1 = g.B[1];
   const int64_t plane = (int64_t)B0 * B1;
   const int64_t total = plane * a.no;
@@ -1060,6 +1093,7 @@ __global__ void k_fix0(FwdArgs<T> a, PadGeom g) {
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void k_full_to_h(const Cx<T>* __restrict__ full, int ncomp, PadGeom g, Cx<T>* __restrict__ H) {
+  pdl_wait();
   const int64_t total = g.nh * ncomp;
   const int B0 = g.B[0], B1 = g.B[1], B2 = g.B[2];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -1076,6 +1110,7 @@ __global__ void k_full_to_h(const Cx<T>* __restrict__ full, int ncomp, PadGeom g
 
 template <typename T>
 __global__ void k_h_to_full(const Cx<T>* __restrict__ H, int ncomp, PadGeom g, Cx<T>* __restrict__ full) {
+  pdl_wait();
   const int B0 = g.B[0], B1 = g.B[1], B2 = g.B[2];
   const int64_t nb = (int64_t)B0 * B1 * B2;
   const int64_t total = nb * ncomp;
@@ -1147,7 +1182,7 @@ void launch_xinv(blr_ctx* c, PadEngine* e, const XPassArgs<T>& a) {
   const size_t sm = sizeof(Cx<T>) * (S::L + (size_t)g.B[0] * t_stride<LPC>() + kPW * S::TILE);
   ensure_smem(k_xinv<T, S>, sm);
   const int nyb = (g.B[1] + LPC - 1) / LPC;
-  k_xinv<T, S><<<a.nx * g.Kz1 * nyb, kPW * 32, sm, c->stream>>>(a, g, e->tw[0]);
+  launch_pdl(k_xinv<T, S>, a.nx * g.Kz1 * nyb, kPW * 32, sm, c->stream, a, g, (const double2*)e->tw[0]);
   BLR_LAUNCHED();
 }
 template <typename T, class S>
@@ -1159,7 +1194,7 @@ void launch_yinv(blr_ctx* c, PadEngine* e, const YPassArgs<T>& a) {
   const size_t sm = sizeof(Cx<T>) * (S::L + (size_t)ntmax * g.B[1] * t_stride<LPC>() + kPW * S::TILE);
   ensure_smem(k_yinv<T, S>, sm);
   const int nxb = (g.P[0] + LPC - 1) / LPC;
-  k_yinv<T, S><<<a.ny * g.Kz1 * nxb, kPW * 32, sm, c->stream>>>(a, g, e->tw[1], ntmax);
+  launch_pdl(k_yinv<T, S>, a.ny * g.Kz1 * nxb, kPW * 32, sm, c->stream, a, g, (const double2*)e->tw[1], ntmax);
   BLR_LAUNCHED();
 }
 template <typename T, class S, int OP>
@@ -1180,7 +1215,7 @@ void launch_lines(blr_ctx* c, PadEngine* e, const LineArgs<T>& a) {
   }
   constexpr int LPC = kZWarps * S::LPW;
   const int nyc = (g.P[1] + LPC - 1) / LPC;
-  k_zlines<T, S, OP><<<g.P[0] * nyc, kZWarps * 32, sm, c->stream>>>(a, g, e->tw[2]);
+  launch_pdl(k_zlines<T, S, OP>, g.P[0] * nyc, kZWarps * 32, sm, c->stream, a, g, (const double2*)e->tw[2]);
   BLR_LAUNCHED();
 }
 template <typename T, class S>
@@ -1192,7 +1227,7 @@ void launch_yfwd(blr_ctx* c, PadEngine* e, const YFwdArgs<T>& a) {
   ensure_smem(k_yfwd<T, S>, sm);
   const int nxb = (g.P[0] + LPC - 1) / LPC;
   const int grid = persistent_grid(k_yfwd<T, S>, kPWF * 32, sm, a.nj * g.Kz1 * nxb);
-  k_yfwd<T, S><<<grid, kPWF * 32, sm, c->stream>>>(a, g, e->tw[1]);
+  launch_pdl(k_yfwd<T, S>, grid, kPWF * 32, sm, c->stream, a, g, (const double2*)e->tw[1]);
   BLR_LAUNCHED();
 }
 template <typename T, class S>
@@ -1204,7 +1239,7 @@ void launch_xfwd(blr_ctx* c, PadEngine* e, const FwdArgs<T>& a) {
   ensure_smem(k_xfwd<T, S>, sm);
   const int nyb = (g.B[1] + LPC - 1) / LPC;
   const int grid = persistent_grid(k_xfwd<T, S>, kPWF * 32, sm, a.no * g.Kz1 * nyb);
-  k_xfwd<T, S><<<grid, kPWF * 32, sm, c->stream>>>(a, g, e->tw[0]);
+  launch_pdl(k_xfwd<T, S>, grid, kPWF * 32, sm, c->stream, a, g, (const double2*)e->tw[0]);
   BLR_LAUNCHED();
 }
 
