@@ -340,7 +340,21 @@ __global__ void __launch_bounds__(kPW * 32) k_yinv(YPassArgs<T> a, PadGeom g, co
     return ok ? acc : cx<T>(0, 0);
   };
   auto store = [&](int line, int y, int, Cx<T> v) { out[line * S::L + y] = v; };
-  wfft<T, S, true>(tile, tw, nl, load, store);
+  if (nt == 1) {
+    // single-term output (the common case): no term loop in the gather
+    const int ax0 = ax[0];
+    const Cx<T>* sl = slab + wl0;
+    auto load1 = [&](int line, int q, int) -> Cx<T> {
+      const int iy = bin_to_index(q, S::L, K1, B1);
+      const int iyc = iy >= 0 ? iy : 0;
+      Cx<T> z = sl[iyc * LPCS + line];
+      if (ax0 >= 1) z = mul_ik<T>(z, ax0 == 1 ? (T)(kTwoPi * (double)freq_of(iyc, K1, B1)) : kzk);
+      return iy >= 0 ? z : cx<T>(0, 0);
+    };
+    wfft<T, S, true>(tile, tw, nl, load1, store);
+  } else {
+    wfft<T, S, true>(tile, tw, nl, load, store);
+  }
 }
 
 // ---------------------------------------------------------------------------
