@@ -262,16 +262,24 @@ __global__ void __launch_bounds__(kPW * 32) k_xinv(XPassArgs<T> a, PadGeom g, co
   if (nl <= 0) return;
   const bool mulx = a.mulx[xf] != 0;
   Cx<T>* out = a.out + xf * g.n1 + ((int64_t)kz * B1 + cky0 + wl0) * S::L;
-  auto load = [&](int line, int p, int) -> Cx<T> {
-    const int ix = bin_to_index(p, S::L, K0, B0);
-    const bool ok = ix >= 0;
-    const int ixc = ok ? ix : 0;
-    Cx<T> z = slab[ixc * LPCS + wl0 + line];
-    if (mulx) z = mul_ik<T>(z, (T)(kTwoPi * (double)freq_of(ixc, K0, B0)));
-    return ok ? z : cx<T>(0, 0);
-  };
+  const Cx<T>* sl = slab + wl0;
   auto store = [&](int line, int x, int, Cx<T> v) { out[line * S::L + x] = v; };
-  wfft<T, S, true>(tile, tw, nl, load, store);
+  if (mulx) {  // uniform per CTA: two gathers instead of a per-element branch
+    auto load = [&](int line, int p, int) -> Cx<T> {
+      const int ix = bin_to_index(p, S::L, K0, B0);
+      const int ixc = ix >= 0 ? ix : 0;
+      const Cx<T> z = mul_ik<T>(sl[ixc * LPCS + line], (T)(kTwoPi * (double)freq_of(ixc, K0, B0)));
+      return ix >= 0 ? z : cx<T>(0, 0);
+    };
+    wfft<T, S, true>(tile, tw, nl, load, store);
+  } else {
+    auto load = [&](int line, int p, int) -> Cx<T> {
+      const int ix = bin_to_index(p, S::L, K0, B0);
+      const Cx<T> z = sl[(ix >= 0 ? ix : 0) * LPCS + line];
+      return ix >= 0 ? z : cx<T>(0, 0);
+    };
+    wfft<T, S, true>(tile, tw, nl, load, store);
+  }
 }
 
 // ---------------------------------------------------------------------------
