@@ -89,6 +89,7 @@ __device__ __forceinline__ void cp_async(Cx<T>* dst, const Cx<T>* src) {
 // trigger at grid exit still removes the launch gap between kernels
 // (-1.1 ms per deformation GN HVP, the same as replaying a CUDA graph).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args&&... args) {
@@ -841,6 +842,7 @@ __global__ void __launch_bounds__(kPWF * 32, 4) k_yfwd(YFwdArgs<T> a, PadGeom g,
   };
   load_tw<T>(tw, twg, S::L);
   int it = blockIdx.x, t = 0, b = 0;
+  pdl_trigger();  // persistent grid: every CTA is already resident
   pdl_wait();
   if (it < nitems) issue(it, 0, 0);
   stg.commit();
@@ -1037,6 +1039,7 @@ __global__ void __launch_bounds__(kPWF * 32, 3) k_xfwd(FwdArgs<T> a, PadGeom g, 
   };
   load_tw<T>(tw, twg, S::L);
   int it = blockIdx.x, t = 0, b = 0;
+  pdl_trigger();  // persistent grid: every CTA is already resident
   pdl_wait();
   if (it < nitems) issue(it, 0, 0);
   stg.commit();
