@@ -500,16 +500,23 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
   const int nst = Tr::acc ? a.nst : 0;
   const size_t warp_bytes = sizeof(Cx<T>) * ((size_t)S::TILE + stage_n) +
                             sizeof(T) * (size_t)(nreal + nst) * S::LPW * L;
+  // fp64: twiddles straight from the engine's global table (L1-resident), which
+  // keeps the CTA's shared footprint at 6 CTAs per SM; fp32 converts into smem
+  constexpr bool kTwG = sizeof(T) == 8;
+  constexpr int kTwN = kTwG ? 0 : L;
   Cx<T>* tw = (Cx<T>*)smem_raw;
-  unsigned char* wb = smem_raw + sizeof(Cx<T>) * L + warp * warp_bytes;
+  const Cx<T>* twp = kTwG ? reinterpret_cast<const Cx<T>*>(twz_g) : tw;
+  unsigned char* wb = smem_raw + sizeof(Cx<T>) * kTwN + warp * warp_bytes;
   Cx<T>* tile = (Cx<T>*)wb;
   Cx<T>* stage = tile + S::TILE;
   Cx<T>* xbuf = stage;
   T* Vst = (T*)(stage + stage_n);
   T* Rsm = Vst + nst * S::LPW * L;
   const int ldR = S::LPW * L;
-  load_tw<T>(tw, twz_g, L);
-  __syncthreads();
+  if constexpr (!kTwG) {
+    load_tw<T>(tw, twz_g, L);
+    __syncthreads();
+  }
   pdl_wait();
   const int nl = min(S::LPW, P1 - y0);
   if (nl <= 0) return;
@@ -679,7 +686,7 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
         for (int o = 0; o < NOM; ++o) acc[o][k2] += c1[o] * p1 + c2[o] * p2;
       }
     };
-    wfft<T, S, true>(tile, tw, nl, load, store);
+    wfft<T, S, true>(tile, twp, nl, load, store);
     if constexpr (OP == kOpContract) {
       if (p == npair - 1) {
         // node complete: rho_n is realized in Rsm.  Stream the cached D(phi_n)
@@ -777,7 +784,7 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
       }
     };
     auto store = [&](int line, int k, int, Cx<T> v) { xbuf[line * L + k] = v; };
-    wfft<T, S, false>(tile, tw, nl, load, store);
+    wfft<T, S, false>(tile, twp, nl, load, store);
     Cx<T>* O1 = a.sout[o] + sline;
     Cx<T>* O2 = two ? a.sout[o + 1] + sline : nullptr;
     for (int idx = lane; idx < S::LPW * Kz1; idx += 32) {
@@ -1231,7 +1238,7 @@ void launch_lines(blr_ctx* c, PadEngine* e, const LineArgs<T>& a) {
   const size_t stage_n = std::max<size_t>(4 * (size_t)(g.Kz1 + 1) * S::LPW, (size_t)S::LPW * S::L);
   const size_t warp_bytes = sizeof(Cx<T>) * ((size_t)S::TILE + stage_n) +
                             sizeof(T) * (size_t)(nreal + nst) * S::LPW * S::L;
-  const size_t sm = S::L * sizeof(Cx<T>) + kZWarps * warp_bytes;
+  const size_t sm = (sizeof(T) == 8 ? 0 : S::L * sizeof(Cx<T>)) + kZWarps * warp_bytes;
   if (sm > (size_t)e->line_smem_max) throw Error(1, "z-line kernel shared memory exceeds the device limit");
   static bool attr_done[2] = {false, false};
   if (!attr_done[sizeof(T) == 8 ? 0 : 1]) {
