@@ -495,8 +495,9 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
   const int nreal = OP == kOpContract ? a.d : (Tr::acc || OP == kOpRealize) ? 0 : ns_blk;
   // shared layout: tw | per warp { tile | stage[max(2*2*Kz1*LPW, LPW*L)] (xbuf aliases it after the
   //                                 C2R phase) | Vst[nst][LPW*L] | Rsm[nreal][LPW*L] }
-  const int fstride = (Kz1 + 1) * S::LPW;  // per-field stage: Kz1 spectra rows + one zero row
-  const int stage_n = max(2 * 2 * fstride, S::LPW * L);
+  const int fstride = Kz1 * S::LPW;  // per-field stage: Kz1 spectra rows
+  const int zoff = 4 * fstride;       // one zero row shared by both buffers and fields
+  const int stage_n = max(zoff + S::LPW, S::LPW * L);
   const int nst = Tr::acc ? a.nst : 0;
   const size_t warp_bytes = sizeof(Cx<T>) * ((size_t)S::TILE + stage_n) +
                             sizeof(T) * (size_t)(nreal + nst) * S::LPW * L;
@@ -552,19 +553,16 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
 #pragma unroll
     for (int n1 = 0; n1 < S::R1; ++n1) {
       const int k = S::R2 * n1 + n2;
-      int row = Kz1, sgn = 1;  // zero row
+      int row = -1, sgn = 1;  // out of band: the shared zero row
       if (k == 0) { row = 0; sgn = 0; }
       else if (k <= K2) { row = k; sgn = 1; }
       else if (k >= L - K2) { row = L - k; sgn = -1; }
-      hidx[n1] = row * S::LPW;
+      hidx[n1] = row < 0 ? -1 : row * S::LPW;
       hsg[n1] = sgn;
     }
   }
-  // zero rows of both stage buffers (never overwritten by the prefetch)
-  for (int i = lane; i < 4 * S::LPW; i += 32) {
-    const int b = i / (2 * S::LPW), q = i - b * 2 * S::LPW;
-    stage[b * 2 * fstride + (q / S::LPW) * fstride + Kz1 * S::LPW + (q % S::LPW)] = cx<T>(0, 0);
-  }
+  // the shared zero row (never overwritten by the prefetch)
+  if (lane < S::LPW) stage[zoff + lane] = cx<T>(0, 0);
   const int npair = (ns_blk + 1) / 2;
   const int nloop = OP == kOpContract ? a.n_nodes : 1;
   const int total = nloop * npair;
@@ -642,8 +640,7 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
     const int node = q / npair, p = q - node * npair;
     const int f = 2 * p;
     const bool two = f + 1 < ns_blk;
-    const Cx<T>* st1 = stage + (q & 1) * 2 * fstride;
-    const Cx<T>* st2 = st1 + fstride;
+    const int st1o = (q & 1) * 2 * fstride, st2o = st1o + fstride;
     // ACC ops: per-pair output coefficients (uniform), applied in the FFT store
     T c1[NOM], c2[NOM];
     const T* V1 = Vst;
@@ -661,8 +658,9 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
     }
     auto load = [&](int line, int, int n1) -> Cx<T> {
       // branch-free Hermitian packing of F1 + i F2 (zero rows index the zero pad row)
-      const Cx<T> F1 = st1[hidx[n1] + line];
-      const Cx<T> F2 = st2[hidx[n1] + line];
+      const int h = hidx[n1];
+      const Cx<T> F1 = stage[(h >= 0 ? st1o + h : zoff) + line];
+      const Cx<T> F2 = stage[(h >= 0 ? st2o + h : zoff) + line];
       const T sg = (T)hsg[n1];
       return cx<T>(F1.x - sg * F2.y, sg * F1.y + F2.x);
     };
@@ -1235,7 +1233,7 @@ void launch_lines(blr_ctx* c, PadEngine* e, const LineArgs<T>& a) {
   const int ns_blk = OP == kOpContract ? a.d : a.ns;
   const int nreal = OP == kOpContract ? a.d : (ZOp<OP>::acc || OP == kOpRealize) ? 0 : ns_blk;
   const int nst = ZOp<OP>::acc ? a.nst : 0;
-  const size_t stage_n = std::max<size_t>(4 * (size_t)(g.Kz1 + 1) * S::LPW, (size_t)S::LPW * S::L);
+  const size_t stage_n = std::max<size_t>(4 * (size_t)g.Kz1 * S::LPW + S::LPW, (size_t)S::LPW * S::L);
   const size_t warp_bytes = sizeof(Cx<T>) * ((size_t)S::TILE + stage_n) +
                             sizeof(T) * (size_t)(nreal + nst) * S::LPW * S::L;
   const size_t sm = (sizeof(T) == 8 ? 0 : S::L * sizeof(Cx<T>)) + kZWarps * warp_bytes;
