@@ -324,7 +324,6 @@ static void fwd2d(blr_ctx* c, PadEngine* e, const std::vector<FwdSpec<T>>& outs,
     ProfScope ps(c, "pad_ypass_fwd", ((double)nterm * g.ns + a.nj * g.n1) * sizeof(Cx<T>));
     dispatch_yfwd<T>(c, e, a);
   }
-  Cx<T>* z0 = (Cx<T>*)e_scratch(c, e, 2, outs.size() * (size_t)g.B[0] * g.B[1] * sizeof(Cx<T>));
   for (size_t off = 0; off < outs.size(); off += kMaxFwd) {
     FwdArgs<T> a;
     std::memset(&a, 0, sizeof(a));
@@ -344,7 +343,6 @@ static void fwd2d(blr_ctx* c, PadEngine* e, const std::vector<FwdSpec<T>>& outs,
     }
     a.in = I;
     a.scale = (T)(1.0 / (double)g.np);
-    a.z0 = z0 + (int64_t)off * g.B[0] * g.B[1];
     const int64_t shift = (int64_t)off * g.nh;
     a.kout = kout ? kout + shift : nullptr;
     a.rk_s = rk.s;
@@ -357,9 +355,6 @@ static void fwd2d(blr_ctx* c, PadEngine* e, const std::vector<FwdSpec<T>>& outs,
       ProfScope ps(c, "pad_xpass_fwd", ((double)nterm * g.n1 + a.no * g.nh * (rk.s ? 4 : 2)) * sizeof(Cx<T>));
       dispatch_xfwd<T>(c, e, a);
     }
-    const int64_t n0 = (int64_t)a.no * g.B[0] * g.B[1];
-    launch_pdl(k_fix0<T>, grid_blocks(n0, 256), 256, 0, c->stream, a, g);
-    BLR_LAUNCHED();
   }
 }
 

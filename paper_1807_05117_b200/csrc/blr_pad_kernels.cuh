@@ -13,7 +13,6 @@
 //   k_yfwd    forward y FFT, band ky kept -> I
 //   k_xfwd    forward x FFT, band kx kept, post-transform multipliers (flux
 //             divergence), 1/P^3, -(v + .) / negation, fused RK4 stage update
-//   k_fix0    the kz = 0 plane: Hermitian symmetrization + the same epilogue
 //
 // Band state lives in the "H layout" [comp][kz 0..K][kx][ky] (Hermitian half);
 // node records are converted back to the reference's full blocks.
@@ -898,7 +897,7 @@ __global__ void __launch_bounds__(kPWF * 32, 4) k_yfwd(YFwdArgs<T> a, PadGeom g,
 
 // ---------------------------------------------------------------------------
 // forward x pass + epilogue: I [..][kz][ky][x] -> band, multipliers, 1/P^3,
-// -(v + .) / negation, fused RK4 stage update (kz = 0 deferred to k_fix0)
+// -(v + .) / negation, fused RK4 stage update (kz = 0 symmetrized in-item)
 // ---------------------------------------------------------------------------
 constexpr int kMaxFwd = 18;
 enum FwdMode { kEpiPlain = 0, kEpiNeg = 1, kEpiNegAdd = 2 };
@@ -918,7 +917,6 @@ struct FwdArgs {
   int no;
   const Cx<T>* in;  // I layout
   T scale;
-  Cx<T>* z0;        // [no][B0*B1] raw kz = 0 plane
   Cx<T>* kout;      // H layout [no][nh] or nullptr
   int rk_s;         // 0: no RK4 update
   T cs, h6;
@@ -963,23 +961,25 @@ __device__ __forceinline__ void epilogue(const FwdArgs<T>& a, const FwdOut<T>& O
 // tile res[ix][LPCS]: consecutive threads take consecutive ky (coalesced), and
 // each thread issues the operand loads of U elements before any store, so the
 // RK4 read-modify-write costs one memory latency per U elements, not one each.
-template <typename T, int LPC, int LPCS>
-__device__ __forceinline__ void epilogue_block(const FwdArgs<T>& a, const FwdOut<T>& O, int o, int kz,
-                                               int cky0, int nlc, const PadGeom& g, const Cx<T>* res) {
+// elem(ix, l, e, r) -> false for an empty slot, else the element's flat
+// H-layout index e and its (scaled) result r.
+template <typename T, int LPC, class Elem>
+__device__ __forceinline__ void epilogue_block(const FwdArgs<T>& a, const FwdOut<T>& O, int o, const PadGeom& g,
+                                               Elem elem) {
   constexpr int U = 2;
-  const int B0 = g.B[0], B1 = g.B[1];
+  const int B0 = g.B[0];
   const int n = B0 * LPC;
   const int s = a.rk_s;
   for (int i0 = threadIdx.x; i0 < n; i0 += U * blockDim.x) {
     Cx<T> r[U], v[U], cc[U], ac[U];
     int64_t e[U];
+    bool ok[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = i0 + u * blockDim.x;
       const int ix = i / LPC, l = i - (i / LPC) * LPC;  // compile-time divisor
-      if (i >= n || l >= nlc) continue;
-      e[u] = ((int64_t)kz * B0 + ix) * B1 + cky0 + l;
-      r[u] = cscale(res[ix * LPCS + l], a.scale);
+      ok[u] = i < n && elem(ix, l, e[u], r[u]);
+      if (!ok[u]) continue;
       const int64_t h = (int64_t)o * g.nh + e[u];
       if (O.mode == kEpiNegAdd) v[u] = O.vt[e[u]];
       if (s) cc[u] = a.cur[h];
@@ -987,8 +987,7 @@ __device__ __forceinline__ void epilogue_block(const FwdArgs<T>& a, const FwdOut
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int i = i0 + u * blockDim.x;
-      if (i >= n || i - (i / LPC) * LPC >= nlc) continue;
+      if (!ok[u]) continue;
       const int64_t h = (int64_t)o * g.nh + e[u];
       Cx<T> k;
       if (O.mode == kEpiNegAdd) k = cx<T>(-(v[u].x + r[u].x), -(v[u].y + r[u].y));
@@ -1014,33 +1013,75 @@ __device__ __forceinline__ void epilogue_block(const FwdArgs<T>& a, const FwdOut
   }
 }
 
+// kz > 0 items: LPC consecutive ky lines.  kz = 0 items pair every ky line
+// with its mirror -ky (warp 0: units p0.., warp 1: their mirrors), so the
+// Hermitian symmetrization of the kz = 0 plane (the reference's symmetrize)
+// happens inside the item: no separate fix-up kernel.
 template <typename T, class S>
 __global__ void __launch_bounds__(kPWF * 32, 3) k_xfwd(FwdArgs<T> a, PadGeom g, const double2* __restrict__ twg) {
+  static_assert(kPWF == 2, "kz = 0 mirror items use one warp per half");
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int LPC = kPWF * S::LPW;
+  constexpr int LPW = S::LPW;
+  constexpr int LPC = kPWF * LPW;
   constexpr int LS = row_stride<T, S, true>();
   constexpr int LPCS = t_stride<LPC>();
   constexpr int SLAB = LPC * LS;
-  const int K0 = g.K[0], B0 = g.B[0], B1 = g.B[1];
+  const int K0 = g.K[0], B0 = g.B[0], B1 = g.B[1], K1 = g.K[1];
   Cx<T>* tw = (Cx<T>*)smem_raw;
   Cx<T>* slab = tw + S::L;                       // [2][LPC][LS] (persistent, as k_yfwd)
   Cx<T>* res = slab + 2 * SLAB;                  // [B0][LPCS] finished block
   const int nyb = (B1 + LPC - 1) / LPC;
-  const int per = g.Kz1 * nyb;
+  const int n0 = (K1 + 1 + LPW - 1) / LPW;      // kz = 0 items (LPW mirror units each)
+  const int per = n0 + (g.Kz1 - 1) * nyb;
   const int nitems = a.no * per;
+  // item r of an output -> kz, first ky (kz > 0) or first unit p0 and the two half sizes (kz = 0)
+  struct Item { int kz, cky0, p0, c1, c2; };
+  auto decode = [&](int r) -> Item {
+    Item m;
+    if (r < n0) {
+      m.kz = 0;
+      m.cky0 = 0;
+      m.p0 = r * LPW;
+      m.c1 = min(LPW, K1 + 1 - m.p0);
+      m.c2 = m.p0 == 0 ? m.c1 - 1 : m.c1;  // unit 0 (ky = 0) is its own mirror
+    } else {
+      const int q = r - n0;
+      m.kz = 1 + q / nyb;
+      m.cky0 = (q - (q / nyb) * nyb) * LPC;
+      m.p0 = -1;
+      m.c1 = min(LPC, B1 - m.cky0);
+      m.c2 = 0;
+    }
+    return m;
+  };
+  // kz = 0: ky index of slot s, and the slot holding its mirror
+  auto slot_iy = [&](const Item& m, int s) -> int {
+    if (s < LPW) return m.p0 + s;
+    return B1 - (m.p0 + (s - LPW) + (m.p0 == 0 ? 1 : 0));
+  };
+  auto mirror_slot = [&](const Item& m, int s) -> int {
+    const int z = m.p0 == 0 ? 1 : 0;
+    if (s < LPW) return (m.p0 + s == 0) ? 0 : LPW + s - z;
+    return s - LPW + z;
+  };
   __shared__ uint64_t bars[2];
   Stager<T> stg;
   stg.init(bars);
   __syncthreads();
   auto issue = [&](int it, int t, int b) {
     const int o = it / per;
-    const int r = it - o * per;
-    const int kz = r / nyb;
-    const int cky0 = (r - kz * nyb) * LPC;
-    const int nlc = min(LPC, B1 - cky0);
-    const Cx<T>* src = a.in + a.o[o].f[t] * g.n1 + ((int64_t)kz * B1 + cky0) * S::L;
-    stg.begin(b, (uint32_t)(nlc * S::L * sizeof(Cx<T>)));
-    stg.rows(slab + b * SLAB, LS, src, S::L, nlc, S::L, b);
+    const Item m = decode(it - o * per);
+    const Cx<T>* base = a.in + a.o[o].f[t] * g.n1 + (int64_t)m.kz * B1 * S::L;
+    Cx<T>* dst = slab + b * SLAB;
+    if (m.kz > 0) {
+      stg.begin(b, (uint32_t)(m.c1 * S::L * sizeof(Cx<T>)));
+      stg.rows(dst, LS, base + (int64_t)m.cky0 * S::L, S::L, m.c1, S::L, b);
+    } else {
+      stg.begin(b, (uint32_t)((m.c1 + m.c2) * S::L * sizeof(Cx<T>)));
+      stg.rows(dst, LS, base + (int64_t)m.p0 * S::L, S::L, m.c1, S::L, b);
+      if (m.c2 > 0)  // mirrors, descending ky
+        stg.rows(dst + LPW * LS, LS, base + (int64_t)slot_iy(m, LPW) * S::L, -(int64_t)S::L, m.c2, S::L, b);
+    }
   };
   load_tw<T>(tw, twg, S::L);
   int it = blockIdx.x, t = 0, b = 0;
@@ -1048,7 +1089,8 @@ __global__ void __launch_bounds__(kPWF * 32, 3) k_xfwd(FwdArgs<T> a, PadGeom g, 
   pdl_wait();
   if (it < nitems) issue(it, 0, 0);
   stg.commit();
-  const int wl0 = (threadIdx.x >> 5) * S::LPW;
+  const int warp = threadIdx.x >> 5;
+  const int wl0 = warp * LPW;
   __syncthreads();  // twiddles
   while (it < nitems) {
     const int o = it / per;
@@ -1059,11 +1101,9 @@ __global__ void __launch_bounds__(kPWF * 32, 3) k_xfwd(FwdArgs<T> a, PadGeom g, 
     if (nit < nitems) issue(nit, ntt, b ^ 1);
     stg.commit();
     stg.wait(b);
-    const int r = it - o * per;
-    const int kz = r / nyb;
-    const int cky0 = (r - kz * nyb) * LPC;
-    const int nl = min(S::LPW, min(LPC, B1 - cky0) - wl0);
-    const int ky0 = cky0 + wl0;
+    const Item m = decode(it - o * per);
+    const int kz = m.kz;
+    const int nl = kz > 0 ? min(LPW, m.c1 - wl0) : (warp == 0 ? m.c1 : m.c2);
     if (nl > 0) {
       const T kzk = (T)(kTwoPi * (double)kz);
       const Cx<T>* sl = slab + b * SLAB + wl0 * LS;
@@ -1072,9 +1112,14 @@ __global__ void __launch_bounds__(kPWF * 32, 3) k_xfwd(FwdArgs<T> a, PadGeom g, 
       auto store = [&](int line, int q, int, Cx<T> v) {
         const int ix = bin_to_index(q, S::L, K0, B0);
         if (ix < 0) return;
-        if (ax == 0) v = mul_ik<T>(v, (T)(kTwoPi * (double)freq_of(ix, K0, B0)));
-        else if (ax == 1) v = mul_ik<T>(v, (T)(kTwoPi * (double)freq_of(ky0 + line, g.K[1], B1)));
-        else if (ax == 2) v = mul_ik<T>(v, kzk);
+        if (ax == 0) {
+          v = mul_ik<T>(v, (T)(kTwoPi * (double)freq_of(ix, K0, B0)));
+        } else if (ax == 1) {
+          const int iy = kz > 0 ? m.cky0 + wl0 + line : slot_iy(m, wl0 + line);
+          v = mul_ik<T>(v, (T)(kTwoPi * (double)freq_of(iy, K1, B1)));
+        } else if (ax == 2) {
+          v = mul_ik<T>(v, kzk);
+        }
         Cx<T>* rp = res + ix * LPCS + wl0 + line;  // owned by this lane for every term
         *rp = t == 0 ? v : cadd(*rp, v);
       };
@@ -1082,39 +1127,29 @@ __global__ void __launch_bounds__(kPWF * 32, 3) k_xfwd(FwdArgs<T> a, PadGeom g, 
     }
     if (t == nt - 1) {
       __syncthreads();
-      const int nlc = min(LPC, B1 - cky0);
       if (kz == 0) {
-        for (int i = threadIdx.x; i < B0 * LPC; i += blockDim.x) {
-          const int ix = i / LPC, l = i - (i / LPC) * LPC;
-          if (l < nlc) a.z0[(int64_t)o * B0 * B1 + ix * B1 + cky0 + l] = cscale(res[ix * LPCS + l], a.scale);
-        }
+        // symmetrize (kx, ky) with (-kx, -ky) inside the item, then the epilogue
+        epilogue_block<T, LPC>(a, O, o, g, [&](int ix, int sl, int64_t& e, Cx<T>& r) {
+          if (sl < LPW ? sl >= m.c1 : sl - LPW >= m.c2) return false;
+          const int mix = ix == 0 ? 0 : B0 - ix;
+          const Cx<T> p = res[ix * LPCS + sl], q = res[mix * LPCS + mirror_slot(m, sl)];
+          r = cx<T>((T)0.5 * a.scale * (p.x + q.x), (T)0.5 * a.scale * (p.y - q.y));
+          e = (int64_t)ix * B1 + slot_iy(m, sl);
+          return true;
+        });
       } else {
-        epilogue_block<T, LPC, LPCS>(a, O, o, kz, cky0, nlc, g, res);
+        epilogue_block<T, LPC>(a, O, o, g, [&](int ix, int l, int64_t& e, Cx<T>& r) {
+          if (l >= m.c1) return false;
+          e = ((int64_t)kz * B0 + ix) * B1 + m.cky0 + l;
+          r = cscale(res[ix * LPCS + l], a.scale);
+          return true;
+        });
       }
     }
     __syncthreads();
     it = nit;
     t = ntt;
     b ^= 1;
-  }
-}
-
-// kz = 0 plane: symmetrize pairs (k, -k), then the same epilogue
-template <typename T>
-__global__ void k_fix0(FwdArgs<T> a, PadGeom g) {
-  pdl_wait();
-  const int B0 = g.B[0], B1 = g.B[1];
-  const int64_t plane = (int64_t)B0 * B1;
-  const int64_t total = plane * a.no;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int o = (int)(i / plane);
-    const int e = (int)(i - o * plane);
-    const int ix = e / B1, iy = e - ix * B1;
-    const int mx = ix == 0 ? 0 : B0 - ix, my = iy == 0 ? 0 : B1 - iy;
-    const int e2 = mx * B1 + my;
-    const Cx<T> p = a.z0[o * plane + e], q = a.z0[o * plane + e2];
-    const Cx<T> r = cx<T>((T)0.5 * (p.x + q.x), (T)0.5 * (p.y - q.y));
-    epilogue<T>(a, a.o[o], (int64_t)o * g.nh + e, e, r);
   }
 }
 
@@ -1268,7 +1303,8 @@ void launch_xfwd(blr_ctx* c, PadEngine* e, const FwdArgs<T>& a) {
                                      (size_t)g.B[0] * t_stride<LPC>());
   ensure_smem(k_xfwd<T, S>, sm);
   const int nyb = (g.B[1] + LPC - 1) / LPC;
-  const int grid = persistent_grid(k_xfwd<T, S>, kPWF * 32, sm, a.no * g.Kz1 * nyb);
+  const int n0 = (g.K[1] + 1 + S::LPW - 1) / S::LPW;
+  const int grid = persistent_grid(k_xfwd<T, S>, kPWF * 32, sm, a.no * (n0 + (g.Kz1 - 1) * nyb));
   launch_pdl(k_xfwd<T, S>, grid, kPWF * 32, sm, c->stream, a, g, (const double2*)e->tw[0]);
   BLR_LAUNCHED();
 }
