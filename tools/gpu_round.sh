@@ -9,5 +9,5 @@ python bench.py --steps 2 --warmup 3 --registration 0 --cpu-baseline 0 > gpurun_
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 2 --warmup 3 --registration 0 --cpu-baseline 0 > gpurun_out/ncu_launch.log 2>&1
 python bench.py --profile-only > gpurun_out/plain2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:int\)(2|6)>\(blr::LineArgs" -s 6 -c 2 -o gpurun_out/dominant python bench.py --profile-only > gpurun_out/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:int\)2>\(blr::LineArgs" -s 2 -c 1 -o gpurun_out/dominant python bench.py --profile-only > gpurun_out/ncu_full.log 2>&1
 echo done
