@@ -109,7 +109,8 @@ int blr_forward_map(blr_ctx* ctx, const void* v, int n_stored, int n_steps, int 
 int blr_inverse_map_and_volume(blr_ctx* ctx, const void* v, int n_stored, int n_steps,
                                int substeps, void* psi_nodes, void* vol_nodes);
 /* tangents (transport.py:386-432).  flags: bit0 = forward pair (dphi),
- * bit1 = backward pair (dpsi), bit2 = volume pair (dvol, needs bit1).
+ * bit1 = backward pair (dpsi), bit2 = volume pair (dvol, needs bit1),
+ * bit3 = record only the final forward node (dphi_nodes holds one node).
  * du_cache (nullable) from blr_forward_map with the same v and substeps. */
 int blr_state_tangents(blr_ctx* ctx, const void* v, const void* dv, int n_stored, int n_steps,
                        int substeps, int flags, const void* du_cache, void* dphi_nodes,

@@ -483,7 +483,8 @@ struct VelBank2 {
 struct Rec2 {
   int comp0;   // first H component
   int ncomp;
-  void* dst;   // full blocks [n_steps+1][ncomp][nb]
+  void* dst;   // full blocks [n_steps+1][ncomp][nb] ([1][ncomp][nb] when final_only)
+  bool final_only = false;
 };
 
 template <typename T, typename Rhs>
@@ -496,10 +497,13 @@ static void rk4_v2(blr_ctx* c, PadEngine* e, int n_steps, int substeps, bool for
   const double dt = (forward ? 1.0 : -1.0) / n;
   const double h = dt / substeps;
   const int64_t nb = c->g.nb();
+  const int last = forward ? n : 0;
   auto record = [&](int node) {
-    for (const auto& r : rec)
-      if (r.dst)
-        h_to_full<T>(c, e, cur + r.comp0 * e->g.nh, r.ncomp, (Cx<T>*)r.dst + (int64_t)node * r.ncomp * nb);
+    for (const auto& r : rec) {
+      if (!r.dst || (r.final_only && node != last)) continue;
+      const int64_t slot = r.final_only ? 0 : node;
+      h_to_full<T>(c, e, cur + r.comp0 * e->g.nh, r.ncomp, (Cx<T>*)r.dst + slot * r.ncomp * nb);
+    }
   };
   record(forward ? 0 : n);
   int si = 0;
@@ -650,7 +654,7 @@ bool state_tangents_v2(blr_ctx* c, FlowRef v, FlowRef dv, int substeps, int flag
     Cx<T>* S = tmp.get<Cx<T>>(nsi * pg.ns);
     Cx<T>* So = tmp.get<Cx<T>>(2 * d * pg.ns);
     const int du0 = cached ? 0 : d;
-    rk4_v2<T>(c, e, v.n_steps, substeps, true, cur, ncomp, {{du0, d, dphi}}, tmp,
+    rk4_v2<T>(c, e, v.n_steps, substeps, true, cur, ncomp, {{du0, d, dphi, (flags & 8) != 0}}, tmp,
               [&](int si, double t, const Cx<T>* s, const Rk& rk) {
                 const auto& vt = V.at(t);
                 const auto& dvt = dV.at(t);

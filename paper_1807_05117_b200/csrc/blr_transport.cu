@@ -366,6 +366,17 @@ template <typename T>
 void state_tangents(blr_ctx* c, FlowRef v, FlowRef dv, int substeps, int flags, const T* du_cache,
                     Cx<T>* dphi, Cx<T>* dpsi, Cx<T>* dvol) {
   if (state_tangents_v2<T>(c, v, dv, substeps, flags, du_cache, dphi, dpsi, dvol)) return;
+  if ((flags & 8) && dphi && (flags & 1)) {
+    // final forward node only: run the recording path into a temporary and keep the last node
+    const int64_t node = (int64_t)c->g.d * c->g.nb();
+    Cx<T>* all = nullptr;
+    BLR_CUDA(cudaMallocAsync((void**)&all, (size_t)(v.n_steps + 1) * node * sizeof(Cx<T>), c->stream));
+    state_tangents<T>(c, v, dv, substeps, flags & ~8, du_cache, all, dpsi, dvol);
+    BLR_CUDA(cudaMemcpyAsync(dphi, all + (int64_t)v.n_steps * node, node * sizeof(Cx<T>),
+                             cudaMemcpyDeviceToDevice, c->stream));
+    BLR_CUDA(cudaFreeAsync(all, c->stream));
+    return;
+  }
   const Geom& g = c->g;
   const int d = g.d;
   const int64_t nb = g.nb(), np = g.np();

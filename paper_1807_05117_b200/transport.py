@@ -252,14 +252,19 @@ def integrate_inverse_map_and_volume(v: TimeFlow, substeps: int = 1):
 
 def integrate_state_tangents(v: TimeFlow, dv: TimeFlow, substeps: int = 1, with_volume: bool = True,
                              with_inverse: bool = True, with_forward: bool = True,
-                             du_cache: torch.Tensor | None = None):
-    """(dphi, dpsi, dvol) tangent node arrays (transport.py:386-432)."""
+                             du_cache: torch.Tensor | None = None, final_only: bool = False):
+    """(dphi, dpsi, dvol) tangent node arrays (transport.py:386-432).
+
+    ``final_only`` records just the last forward-tangent node (dphi has one
+    node): the Gauss-Newton deformation HVP reads only dphi[-1]."""
     v._check_compatible(dv)
     dom = v.domain
-    dphi = _nodes(dom, v.n_nodes, dom.ndim) if with_forward else None
+    dphi = _nodes(dom, 1 if final_only else v.n_nodes, dom.ndim) if with_forward else None
     dpsi = _nodes(dom, v.n_nodes, dom.ndim) if with_inverse else None
     dvol = _nodes(dom, v.n_nodes, None) if (with_inverse and with_volume) else None
     flags = (1 if with_forward else 0) | (2 if with_inverse else 0) | (4 if dvol is not None else 0)
+    if final_only and with_forward:
+        flags |= 8
     _lib.call("blr_state_tangents", dom.ctx().bind(), ptr(v.values), ptr(dv.values), v.n_stored,
               v.n_steps, int(substeps), flags, ptr(du_cache) if du_cache is not None else None,
               ptr(dphi) if dphi is not None else None, ptr(dpsi) if dpsi is not None else None,
