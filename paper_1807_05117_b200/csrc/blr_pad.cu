@@ -360,13 +360,26 @@ static void fwd2d(blr_ctx* c, PadEngine* e, const std::vector<FwdSpec<T>>& outs,
 
 template <typename T>
 static void full_to_h(blr_ctx* c, PadEngine* e, const Cx<T>* full, int ncomp, Cx<T>* H) {
-  launch_pdl(k_full_to_h<T>, grid_blocks(e->g.nh * ncomp, 256), 256, 0, c->stream, full, ncomp, e->g, H);
+  const PadGeom& g = e->g;
+  const size_t sm = (size_t)g.Kz1 * g.B[1] * sizeof(Cx<T>);
+  if (sm <= 48 * 1024) {
+    launch_pdl(k_full_to_h_t<T>, ncomp * g.B[0], 256, sm, c->stream, full, ncomp, g, H);
+  } else {
+    launch_pdl(k_full_to_h<T>, grid_blocks(g.nh * ncomp, 256), 256, 0, c->stream, full, ncomp, g, H);
+  }
   BLR_LAUNCHED();
 }
 
 template <typename T>
 static void h_to_full(blr_ctx* c, PadEngine* e, const Cx<T>* H, int ncomp, Cx<T>* full) {
-  launch_pdl(k_h_to_full<T>, grid_blocks(c->g.nb() * ncomp, 256), 256, 0, c->stream, H, ncomp, e->g, full);
+  const PadGeom& g = e->g;
+  const size_t sm = 2 * (size_t)g.Kz1 * g.B[1] * sizeof(Cx<T>);
+  if (sm <= 96 * 1024) {
+    ensure_smem(k_h_to_full_t<T>, sm);
+    launch_pdl(k_h_to_full_t<T>, ncomp * g.B[0], 256, sm, c->stream, H, ncomp, g, full);
+  } else {
+    launch_pdl(k_h_to_full<T>, grid_blocks(c->g.nb() * ncomp, 256), 256, 0, c->stream, H, ncomp, g, full);
+  }
   BLR_LAUNCHED();
 }
 

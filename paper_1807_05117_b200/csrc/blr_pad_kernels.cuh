@@ -1156,6 +1156,59 @@ __global__ void __launch_bounds__(kPWF * 32, 3) k_xfwd(FwdArgs<T> a, PadGeom g, 
 // ---------------------------------------------------------------------------
 // layout conversion: full block [comp][kx][ky][kz] <-> H layout [comp][kz][kx][ky]
 // ---------------------------------------------------------------------------
+// Tiled conversions: one CTA per (component, kx) slice; the H rows of the
+// slice (and, for the negative kz half, of its mirror slice -kx) go through
+// shared memory so both the H-layout and the full-block side are row-coalesced.
+template <typename T>
+__global__ void __launch_bounds__(256) k_h_to_full_t(const Cx<T>* __restrict__ H, int ncomp, PadGeom g,
+                                                     Cx<T>* __restrict__ full) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  pdl_wait();
+  const int B0 = g.B[0], B1 = g.B[1], B2 = g.B[2], Kz1 = g.Kz1;
+  const int c = blockIdx.x / B0, ix = blockIdx.x - (blockIdx.x / B0) * B0;
+  const int mx = ix == 0 ? 0 : B0 - ix;
+  Cx<T>* T1 = (Cx<T>*)smem_raw;  // [Kz1][B1] slice ix
+  Cx<T>* T2 = T1 + Kz1 * B1;     // [Kz1][B1] slice -kx
+  const Cx<T>* Hc = H + c * g.nh;
+  for (int i = threadIdx.x; i < Kz1 * B1; i += blockDim.x) {
+    const int kz = i / B1, iy = i - (i / B1) * B1;
+    T1[i] = Hc[((int64_t)kz * B0 + ix) * B1 + iy];
+    T2[i] = Hc[((int64_t)kz * B0 + mx) * B1 + iy];
+  }
+  __syncthreads();
+  Cx<T>* out = full + ((int64_t)c * B0 + ix) * B1 * B2;
+  for (int i = threadIdx.x; i < B1 * B2; i += blockDim.x) {
+    const int iy = i / B2, iz = i - (i / B2) * B2;
+    if (iz < Kz1) {
+      out[i] = T1[iz * B1 + iy];
+    } else {
+      const int my = iy == 0 ? 0 : B1 - iy;
+      out[i] = cconj(T2[(B2 - iz) * B1 + my]);
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_full_to_h_t(const Cx<T>* __restrict__ full, int ncomp, PadGeom g,
+                                                     Cx<T>* __restrict__ H) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  pdl_wait();
+  const int B0 = g.B[0], B1 = g.B[1], B2 = g.B[2], Kz1 = g.Kz1;
+  const int c = blockIdx.x / B0, ix = blockIdx.x - (blockIdx.x / B0) * B0;
+  Cx<T>* Tt = (Cx<T>*)smem_raw;  // [Kz1][B1]
+  const Cx<T>* in = full + ((int64_t)c * B0 + ix) * B1 * B2;
+  for (int i = threadIdx.x; i < B1 * Kz1; i += blockDim.x) {
+    const int iy = i / Kz1, kz = i - (i / Kz1) * Kz1;
+    Tt[kz * B1 + iy] = in[(int64_t)iy * B2 + kz];
+  }
+  __syncthreads();
+  Cx<T>* Hc = H + c * g.nh;
+  for (int i = threadIdx.x; i < Kz1 * B1; i += blockDim.x) {
+    const int kz = i / B1, iy = i - (i / B1) * B1;
+    Hc[((int64_t)kz * B0 + ix) * B1 + iy] = Tt[i];
+  }
+}
+
 template <typename T>
 __global__ void k_full_to_h(const Cx<T>* __restrict__ full, int ncomp, PadGeom g, Cx<T>* __restrict__ H) {
   pdl_wait();
