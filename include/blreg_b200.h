@@ -132,6 +132,15 @@ int blr_momentum_tangent(blr_ctx* ctx, const void* v, const void* dv, int n_stor
 int blr_contract(blr_ctx* ctx, const void* phi_nodes, const void* rho_nodes, int n_nodes,
                  const double* weights, int transpose, void* dphi_cache, int cache_mode,
                  void* out);
+/* backward momentum transport fused with the summed contraction:
+ * out = sum_n w_n (rho_n + project(D(phi_n)^(T|.) rho_n)), rho_n the momentum
+ * nodes of blr_momentum(v, rho_end).  Equals blr_momentum followed by
+ * blr_contract(weights != NULL) without materializing the rho node records
+ * (the Gauss-Newton deformation HVP data term, deformation.py:140-153 +
+ * transport.py:435-445).  weights: n_steps + 1 doubles (host). */
+int blr_momentum_contract(blr_ctx* ctx, const void* v, int n_stored, int n_steps, int substeps,
+                          const void* rho_end, const void* phi_nodes, const double* weights,
+                          int transpose, void* dphi_cache, int cache_mode, void* out);
 /* generic truncated product pi(iota(M) . iota(x)) with optional transpose
  * (spectral.conv_matvec, spectral.py:291-297) for one (d x d, d) pair. */
 int blr_conv_matvec(blr_ctx* ctx, const void* M, const void* x, int transpose, void* out);

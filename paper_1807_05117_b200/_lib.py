@@ -48,6 +48,7 @@ SIGNATURES = {
     "blr_momentum": [_vp, _vp, _i, _i, _i, _vp, _vp],
     "blr_momentum_tangent": [_vp, _vp, _vp, _i, _i, _i, _vp, _vp, _i, _vp, _vp],
     "blr_contract": [_vp, _vp, _vp, _i, _dp, _i, _vp, _i, _vp],
+    "blr_momentum_contract": [_vp, _vp, _i, _i, _i, _vp, _vp, _dp, _i, _vp, _i, _vp],
     "blr_conv_matvec": [_vp, _vp, _vp, _i, _vp],
     "blr_warp": [_vp, _vp, _i, _vp, _i, _i, _vp],
     "blr_grid_gradient": [_vp, _vp, _i, _i, _vp],

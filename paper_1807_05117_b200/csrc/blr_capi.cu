@@ -327,6 +327,20 @@ int blr_contract(blr_ctx* c, const void* phi, const void* rho, int n_nodes, cons
   });
 }
 
+int blr_momentum_contract(blr_ctx* c, const void* v, int n_stored, int n_steps, int substeps,
+                          const void* rho_end, const void* phi, const double* weights, int transpose,
+                          void* dphi_cache, int cache_mode, void* out) {
+  return guarded([&] {
+    need(c && v && rho_end && out && weights && substeps >= 1, "bad arguments");
+    need(cache_mode >= 0 && cache_mode <= 2, "bad cache_mode");
+    need(cache_mode == 0 || dphi_cache, "cache_mode needs a cache buffer");
+    need(cache_mode == 2 || phi, "phi nodes required");
+    FlowRef f = flow(v, n_stored, n_steps);
+    DISPATCH(c, momentum_contract<T>(c, f, substeps, (const Cx<T>*)rho_end, (const Cx<T>*)phi, weights,
+                                     transpose != 0, (T*)dphi_cache, cache_mode, (Cx<T>*)out));
+  });
+}
+
 int blr_conv_matvec(blr_ctx* c, const void* M, const void* x, int transpose, void* out) {
   return guarded([&] {
     need(c && M && x && out, "bad arguments");

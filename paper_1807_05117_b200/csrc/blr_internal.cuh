@@ -79,6 +79,9 @@ template <typename T> void momentum_tangent(blr_ctx* c, FlowRef v, FlowRef dv, i
 template <typename T> void contract(blr_ctx* c, const Cx<T>* phi, const Cx<T>* rho, int n_nodes,
                                     const double* weights, bool transpose, T* dphi_cache, int cache_mode,
                                     Cx<T>* out);
+template <typename T> void momentum_contract(blr_ctx* c, FlowRef v, int substeps, const Cx<T>* rho_end,
+                                             const Cx<T>* phi, const double* weights, bool transpose,
+                                             T* dphi_cache, int cache_mode, Cx<T>* out);
 template <typename T> void conv_matvec(blr_ctx* c, const Cx<T>* M, const Cx<T>* x, bool transpose, Cx<T>* out);
 
 
@@ -95,6 +98,9 @@ template <typename T> bool momentum_pair_v2(blr_ctx* c, FlowRef v, FlowRef dv, i
 template <typename T> bool contract_v2(blr_ctx* c, const Cx<T>* phi, const Cx<T>* rho, int n_nodes,
                                        const double* weights, bool transpose, T* dphi_cache, int cache_mode,
                                        Cx<T>* out);
+template <typename T> bool momentum_contract_v2(blr_ctx* c, FlowRef v, int substeps, const Cx<T>* rho_end,
+                                                const Cx<T>* phi, const double* weights, bool transpose,
+                                                T* dphi_cache, int cache_mode, Cx<T>* out);
 
 // full grid (blr_grid.cu)
 template <typename T> void warp(blr_ctx* c, const T* f, int nimg, const T* disp, int n_disp, int interp, T* out);

@@ -849,18 +849,15 @@ bool momentum_pair_v2(blr_ctx* c, FlowRef v, FlowRef dv, int substeps, const Cx<
 }
 
 // contract: out = sum_i w_i (rho_i + pi(D(phi_i)^T rho_i)) or per node
+// D(phi_i) realizations for the contraction: the cache itself (mode 2), filled
+// (mode 1) or a temporary (mode 0)
 template <typename T>
-bool contract_v2(blr_ctx* c, const Cx<T>* phi, const Cx<T>* rho, int n_nodes, const double* weights,
-                 bool transpose, T* dphi_cache, int cache_mode, Cx<T>* out) {
-  PadEngine* e = engine<T>(c);
-  if (!e) return false;
-  if (n_nodes > 32) return false;
+static T* contract_jacobians(blr_ctx* c, PadEngine* e, const Cx<T>* phi, int n_nodes, T* dphi_cache,
+                             int cache_mode, Tmp2& tmp) {
   const Geom& g = c->g;
   const PadGeom& pg = e->g;
   const int d = g.d, dd = d * d;
-  const int64_t nb = g.nb(), L = d * nb;
-  Tmp2 tmp(c);
-  // D(phi_i) realizations (cache fill or temporary)
+  const int64_t L = d * g.nb();
   T* M = dphi_cache;
   if (cache_mode == 0) M = tmp.get<T>((int64_t)n_nodes * dd * pg.np);
   if (cache_mode != 2) {
@@ -881,6 +878,47 @@ bool contract_v2(blr_ctx* c, const Cx<T>* phi, const Cx<T>* rho, int n_nodes, co
       lines<T, kOpRealize>(c, e, la, sbytes(pg, dd, 0, 0, dd, sizeof(T)));
     }
   }
+  return M;
+}
+
+// sum_n w_n D(phi_n)^(T) rho_n for nodes [node0, node0 + nn) with the rho
+// nodes already realized in S layout (RS [node][d][ns]) -> band H layout Kh
+template <typename T>
+static void contract_core(blr_ctx* c, PadEngine* e, const Cx<T>* RS, const T* M, int node0, int nn,
+                          const double* w, bool transpose, Cx<T>* So, Cx<T>* Kh) {
+  const Geom& g = c->g;
+  const PadGeom& pg = e->g;
+  const int d = g.d, dd = d * d;
+  LineArgs<T> la;
+  std::memset(&la, 0, sizeof(la));
+  la.d = d; la.no = d; la.transpose = transpose ? 1 : 0;
+  la.n_nodes = nn;
+  la.sin_node_stride = (int64_t)d * pg.ns;
+  la.rin_node_stride = (int64_t)dd * pg.np;
+  for (int a = 0; a < d; ++a) la.sin[a] = RS + ((int64_t)node0 * d + a) * pg.ns;
+  for (int k = 0; k < dd; ++k) la.rin[k] = M + ((int64_t)node0 * dd + k) * pg.np;
+  for (int i = 0; i < nn; ++i) la.w[i] = w ? w[i] : 1.0;
+  for (int i = 0; i < d; ++i) la.sout[i] = So + i * pg.ns;
+  lines<T, kOpContract>(c, e, la,
+                        (double)nn * (d * pg.ns * sizeof(Cx<T>) + dd * pg.np * sizeof(T)) +
+                            d * pg.ns * sizeof(Cx<T>));
+  std::vector<FwdSpec<T>> outs;
+  for (int i = 0; i < d; ++i) outs.push_back(fwd1<T>(So + i * pg.ns, kEpiPlain));
+  fwd2d<T>(c, e, outs, Kh, Rk());
+}
+
+template <typename T>
+bool contract_v2(blr_ctx* c, const Cx<T>* phi, const Cx<T>* rho, int n_nodes, const double* weights,
+                 bool transpose, T* dphi_cache, int cache_mode, Cx<T>* out) {
+  PadEngine* e = engine<T>(c);
+  if (!e) return false;
+  if (n_nodes > 32) return false;
+  const Geom& g = c->g;
+  const PadGeom& pg = e->g;
+  const int d = g.d;
+  const int64_t L = d * g.nb();
+  Tmp2 tmp(c);
+  const T* M = contract_jacobians<T>(c, e, phi, n_nodes, dphi_cache, cache_mode, tmp);
   // rho nodes -> S layout (all nodes)
   Cx<T>* RH = tmp.get<Cx<T>>(d * pg.nh);
   Cx<T>* RS = tmp.get<Cx<T>>((int64_t)n_nodes * d * pg.ns);
@@ -897,23 +935,8 @@ bool contract_v2(blr_ctx* c, const Cx<T>* phi, const Cx<T>* rho, int n_nodes, co
   const int nrun = summed ? 1 : n_nodes;
   if (summed) BLR_CUDA(cudaMemsetAsync(out, 0, L * sizeof(Cx<T>), c->stream));
   for (int run = 0; run < nrun; ++run) {
-    LineArgs<T> la;
-    std::memset(&la, 0, sizeof(la));
-    la.d = d; la.no = d; la.transpose = transpose ? 1 : 0;
-    la.n_nodes = summed ? n_nodes : 1;
-    const int node0 = summed ? 0 : run;
-    la.sin_node_stride = (int64_t)d * pg.ns;
-    la.rin_node_stride = (int64_t)dd * pg.np;
-    for (int a = 0; a < d; ++a) la.sin[a] = RS + ((int64_t)node0 * d + a) * pg.ns;
-    for (int k = 0; k < dd; ++k) la.rin[k] = M + ((int64_t)node0 * dd + k) * pg.np;
-    for (int i = 0; i < la.n_nodes; ++i) la.w[i] = summed ? weights[i] : 1.0;
-    for (int i = 0; i < d; ++i) la.sout[i] = So + i * pg.ns;
-    lines<T, kOpContract>(c, e, la,
-                          (double)la.n_nodes * (d * pg.ns * sizeof(Cx<T>) + dd * pg.np * sizeof(T)) +
-                              d * pg.ns * sizeof(Cx<T>));
-    std::vector<FwdSpec<T>> outs;
-    for (int i = 0; i < d; ++i) outs.push_back(fwd1<T>(So + i * pg.ns, kEpiPlain));
-    fwd2d<T>(c, e, outs, Kh, Rk());
+    contract_core<T>(c, e, RS, M, summed ? 0 : run, summed ? n_nodes : 1, summed ? weights : nullptr, transpose,
+                     So, Kh);
     h_to_full<T>(c, e, Kh, d, Kf);
     Cx<T>* o = summed ? out : out + run * L;
     if (summed) {
@@ -927,6 +950,67 @@ bool contract_v2(blr_ctx* c, const Cx<T>* phi, const Cx<T>* rho, int n_nodes, co
   return true;
 }
 
+// Backward momentum transport fused with the summed contraction
+// sum_n w_n (rho_n + project(D(phi_n)^(T) rho_n)): the sweep's own node-time
+// realizations of rho (the first RK4 stage of every step) are written straight
+// into the contraction's S-layout node buffer, and sum_n w_n rho_n accumulates
+// in H layout, so no rho node record is ever materialized or re-transformed.
+template <typename T>
+bool momentum_contract_v2(blr_ctx* c, FlowRef v, int substeps, const Cx<T>* rho_end, const Cx<T>* phi,
+                          const double* weights, bool transpose, T* dphi_cache, int cache_mode, Cx<T>* out) {
+  PadEngine* e = engine<T>(c);
+  if (!e) return false;
+  const int n = v.n_steps, n_nodes = n + 1;
+  if (n_nodes > 32 || !weights) return false;
+  const Geom& g = c->g;
+  const PadGeom& pg = e->g;
+  const int d = g.d, dd = d * d;
+  Tmp2 tmp(c);
+  const T* M = contract_jacobians<T>(c, e, phi, n_nodes, dphi_cache, cache_mode, tmp);
+  VelBank2<T> V(c, e, v, false, tmp);
+  Cx<T>* cur = tmp.get<Cx<T>>(d * pg.nh);
+  full_to_h<T>(c, e, rho_end, d, cur);
+  Cx<T>* RS = tmp.get<Cx<T>>((int64_t)n_nodes * d * pg.ns);
+  Cx<T>* S = tmp.get<Cx<T>>(d * pg.ns);
+  Cx<T>* So = tmp.get<Cx<T>>(dd * pg.ns);
+  Cx<T>* wsum = tmp.get<Cx<T>>(d * pg.nh);  // sum_n w_n rho_n (H layout)
+  BLR_CUDA(cudaMemsetAsync(wsum, 0, d * pg.nh * sizeof(Cx<T>), c->stream));
+  auto realize = [&](const Cx<T>* s, Cx<T>* dst) {
+    std::vector<InvSpec<T>> f;
+    for (int a = 0; a < d; ++a) f.push_back(inv1<T>(s + a * pg.nh, -1));
+    inv2d<T>(c, e, f, dst);
+  };
+  const int per_node = 4 * substeps;
+  rk4_v2<T>(c, e, n, substeps, false, cur, d, {}, tmp, [&](int si, double t, const Cx<T>* s, const Rk& rk) {
+    const auto& vt = V.at(t);
+    Cx<T>* Sd = S;
+    if (si % per_node == 0) {  // first stage of a step: the state is rho at node n - step
+      const int node = n - si / per_node;
+      Sd = RS + (int64_t)node * d * pg.ns;
+      band_axpby<T>(c, weights[node], s, 1.0, wsum, d * pg.nh);
+    }
+    realize(s, Sd);
+    LineArgs<T> la;
+    std::memset(&la, 0, sizeof(la));
+    la.d = d; la.ns = d; la.nr = d; la.no = dd;
+    for (int i = 0; i < d; ++i) la.sin[i] = Sd + i * pg.ns;
+    for (int j = 0; j < d; ++j) la.rin[j] = vt.real + j * pg.np;
+    for (int i = 0; i < dd; ++i) la.sout[i] = So + i * pg.ns;
+    lines<T, kOpOuter>(c, e, la, sbytes(pg, d, d, dd, 0, sizeof(T)));
+    std::vector<FwdSpec<T>> outs;
+    push_flux<T>(g, pg, So, outs);
+    fwd2d<T>(c, e, outs, nullptr, rk);
+  });
+  // node 0 (t = 0) is reached only as the sweep's final state
+  realize(cur, RS);
+  band_axpby<T>(c, weights[0], cur, 1.0, wsum, d * pg.nh);
+  Cx<T>* Kh = tmp.get<Cx<T>>(d * pg.nh);
+  contract_core<T>(c, e, RS, M, 0, n_nodes, weights, transpose, So, Kh);
+  band_axpby<T>(c, 1.0, wsum, 1.0, Kh, d * pg.nh);
+  h_to_full<T>(c, e, Kh, d, out);
+  return true;
+}
+
 #define BLR_PINST(T)                                                                                   \
   template bool pad_engine_ok<T>(blr_ctx*);                                                            \
   template bool forward_map_v2<T>(blr_ctx*, FlowRef, int, Cx<T>*, T*);                                 \
@@ -937,7 +1021,9 @@ bool contract_v2(blr_ctx* c, const Cx<T>* phi, const Cx<T>* rho, int n_nodes, co
   template bool momentum_pair_v2<T>(blr_ctx*, FlowRef, FlowRef, int, const Cx<T>*, const Cx<T>*,       \
                                     Cx<T>*, Cx<T>*);                                                   \
   template bool contract_v2<T>(blr_ctx*, const Cx<T>*, const Cx<T>*, int, const double*, bool, T*, int, \
-                               Cx<T>*);
+                               Cx<T>*);                                                               \
+  template bool momentum_contract_v2<T>(blr_ctx*, FlowRef, int, const Cx<T>*, const Cx<T>*,              \
+                                        const double*, bool, T*, int, Cx<T>*);
 BLR_PINST(double)
 BLR_PINST(float)
 

@@ -584,6 +584,21 @@ void momentum_tangent(blr_ctx* c, FlowRef v, FlowRef dv, int substeps, const Cx<
 // ---------------------------------------------------------------------------
 // Jacobian contraction (deformation.py:63-72) and generic conv_matvec
 // ---------------------------------------------------------------------------
+// backward momentum + summed contraction (the GN deformation HVP data term)
+template <typename T>
+void momentum_contract(blr_ctx* c, FlowRef v, int substeps, const Cx<T>* rho_end, const Cx<T>* phi,
+                       const double* weights, bool transpose, T* dphi_cache, int cache_mode, Cx<T>* out) {
+  if (momentum_contract_v2<T>(c, v, substeps, rho_end, phi, weights, transpose, dphi_cache, cache_mode, out))
+    return;
+  const int64_t node = (int64_t)c->g.d * c->g.nb();
+  const int n_nodes = v.n_steps + 1;
+  Cx<T>* rho = nullptr;
+  BLR_CUDA(cudaMallocAsync((void**)&rho, (size_t)n_nodes * node * sizeof(Cx<T>), c->stream));
+  momentum<T>(c, v, substeps, rho_end, rho);
+  contract<T>(c, phi, rho, n_nodes, weights, transpose, dphi_cache, cache_mode, out);
+  BLR_CUDA(cudaFreeAsync(rho, c->stream));
+}
+
 template <typename T>
 void contract(blr_ctx* c, const Cx<T>* phi, const Cx<T>* rho, int n_nodes, const double* weights,
               bool transpose, T* dphi_cache, int cache_mode, Cx<T>* out) {
@@ -667,6 +682,8 @@ void conv_matvec(blr_ctx* c, const Cx<T>* M, const Cx<T>* x, bool transpose, Cx<
                                     const Cx<T>*, bool, Cx<T>*, Cx<T>*);                       \
   template void contract<T>(blr_ctx*, const Cx<T>*, const Cx<T>*, int, const double*, bool, T*, \
                             int, Cx<T>*);                                                      \
+  template void momentum_contract<T>(blr_ctx*, FlowRef, int, const Cx<T>*, const Cx<T>*,         \
+                                     const double*, bool, T*, int, Cx<T>*);                      \
   template void conv_matvec<T>(blr_ctx*, const Cx<T>*, const Cx<T>*, bool, Cx<T>*);
 BLR_TINST(double)
 BLR_TINST(float)
