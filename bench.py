@@ -238,6 +238,21 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def survey_model_bytes(args, dom):
+    """SURVEY §8(d) / Appendix A.8 algorithmic bytes of one GN HVP at the pad in use:
+    F_pad * 2S(P^3+B^3) + X_full * 2S(N^3+B^3) + G * S*N^3 (no cross-HVP caching)."""
+    S = 8 if args.dtype == "float64" else 4
+    P3 = int(np.prod(dom.pad))
+    B3 = (2 * args.band + 1) ** 3
+    N3 = args.size ** 3
+    nt = args.nt
+    if args.objective == "state":
+        F, X, G = 4 * nt * 24 + 6, 3 + 3 * (nt + 1), 6 + 12 * (nt + 1)
+    else:
+        F, X, G = (4 * nt * 24 + 6) + (4 * nt * 12 + 3) + 15 * (nt + 1), 6, 12
+    return float(F * 2 * S * (P3 + B3) + X * 2 * S * (N3 + B3) + G * S * N3)
+
+
 def ncu_traffic():
     """Per-category DRAM bytes per launch from the committed ncu capture, if any."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -355,6 +370,20 @@ def run_b200(args, rank, world, local):
                 "traffic": tr, "algorithmic_bytes_per_launch": nbytes / n_launch,
                 "avg_launch_us": ms / n_launch * 1e3}
 
+    # whole-HVP view of the metric's "% HBM roofline": the engine's compulsory
+    # bytes per HVP (sum of the per-kernel counts above, with the D(u) / D(phi)
+    # caches) and the SURVEY §8(d) byte model at this pad (no cross-HVP caching)
+    hvp_bytes = sum(v[2] for v in prof.values())
+    model_bytes = survey_model_bytes(args, dom)
+    t_s = per_step_ms * 1e-3
+    roofline_hvp = {"bytes_per_hvp": hvp_bytes, "achieved": round(hvp_bytes / t_s / 1e9, 1),
+                    "frac": round(hvp_bytes / t_s / 1e9 / peak, 4),
+                    "survey_model_bytes": model_bytes,
+                    "survey_model_frac": round(model_bytes / t_s / 1e9 / peak, 4),
+                    "peak": peak, "unit": "GB/s",
+                    "note": "bytes/HVP over the timed ms/HVP; the survey model counts realized pad "
+                            "passes c_pad = 2S(P^3+B^3) without the stage caches"}
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": per_step_ms, "higher_is_better": True,
@@ -365,6 +394,7 @@ def run_b200(args, rank, world, local):
                 "d2h_bytes_per_step": host_out.numel() * host_out.element_size()},
         "gpu_launches": launches,
         "roofline": roofline,
+        "roofline_hvp": roofline_hvp,
         "kernel_breakdown": breakdown,
         "clocks": clocks.summary(),
     }
