@@ -327,25 +327,32 @@ void jacobian_det(blr_ctx* c, const T* u, T* out) {
 // fused objective data terms
 // ---------------------------------------------------------------------------
 // acc[a] = sum_i w_i * (vol_i * dlam(x + psi_i)) * gm_i[a]   (state.py:125-137)
+// node weights travel as a kernel parameter (no host->device copy per call)
+constexpr int kMaxNodeW = 64;
+struct NodeW {
+  double w[kMaxNodeW];
+};
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_state_gn(const T* __restrict__ dlam, const T* __restrict__ vol,
                                                   const T* __restrict__ psi, const T* __restrict__ gm,
-                                                  int n_nodes, const double* __restrict__ w, int interp,
-                                                  FullDesc fd, T* __restrict__ acc) {
+                                                  int n_nodes, NodeW w, int interp,
+                                                  FullDesc fd, int add, T* __restrict__ acc) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < fd.nn;
        i += (int64_t)gridDim.x * blockDim.x) {
     int x[3];
     unravel(fd, i, x);
     T s[3] = {0, 0, 0};
+#pragma unroll 4
     for (int k = 0; k < n_nodes; ++k) {
       double c[3];
       sample_coords<T>(fd, psi + (int64_t)k * fd.d * fd.nn, i, x, c);
       T val = (T)interp_at<T>(dlam, fd, c, interp);
       T lam = vol[(int64_t)k * fd.nn + i] * val;
-      T wk = (T)w[k];
+      T wk = (T)w.w[k];
       for (int a = 0; a < fd.d; ++a) s[a] += wk * (lam * gm[((int64_t)k * fd.d + a) * fd.nn + i]);
     }
-    for (int a = 0; a < fd.d; ++a) acc[a * fd.nn + i] = s[a];
+    for (int a = 0; a < fd.d; ++a) acc[a * fd.nn + i] = add ? acc[a * fd.nn + i] + s[a] : s[a];
   }
 }
 
@@ -353,9 +360,6 @@ template <typename T>
 void state_gn_accumulate(blr_ctx* c, const T* dlam, const T* vol, const T* psi, const T* gm,
                          int n_nodes, const double* weights, int interp, T* acc) {
   FullDesc fd = full_desc(c->g);
-  double* dw = nullptr;
-  BLR_CUDA(cudaMallocAsync((void**)&dw, n_nodes * sizeof(double), c->stream));
-  BLR_CUDA(cudaMemcpyAsync(dw, weights, n_nodes * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   const T* src = dlam;
   T* coef = nullptr;
   if (interp == 3) {
@@ -364,11 +368,16 @@ void state_gn_accumulate(blr_ctx* c, const T* dlam, const T* vol, const T* psi, 
     src = coef;
   }
   ProfScope ps(c, "state_gn_accumulate", (double)fd.nn * (n_nodes * (1 + 2 * fd.d) + 1 + fd.d) * sizeof(T));
-  k_state_gn<T><<<grid_blocks(fd.nn, 256), 256, 0, c->stream>>>(src, vol, psi, gm, n_nodes, dw, interp,
-                                                                 fd, acc);
-  BLR_LAUNCHED();
+  for (int k0 = 0; k0 < n_nodes; k0 += kMaxNodeW) {  // node chunks: weights ride in the parameters
+    const int nk = std::min(kMaxNodeW, n_nodes - k0);
+    NodeW dw;
+    for (int k = 0; k < nk; ++k) dw.w[k] = weights[k0 + k];
+    k_state_gn<T><<<grid_blocks(fd.nn, 256), 256, 0, c->stream>>>(
+        src, vol + (int64_t)k0 * fd.nn, psi + (int64_t)k0 * fd.d * fd.nn, gm + (int64_t)k0 * fd.d * fd.nn, nk, dw,
+        interp, fd, k0 > 0 ? 1 : 0, acc);
+    BLR_LAUNCHED();
+  }
   if (coef) BLR_CUDA(cudaFreeAsync(coef, c->stream));
-  BLR_CUDA(cudaFreeAsync(dw, c->stream));
 }
 
 // out = c * sum_a g[a] u[a]
