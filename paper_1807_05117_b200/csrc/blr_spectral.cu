@@ -198,14 +198,26 @@ __global__ void __launch_bounds__(256) k_scatter(ScatterArgs<T> a, GridDesc gd, 
   using C = Cx<T>;
   const int64_t hs = gd.half_size();
   const int64_t total = hs * a.nf;
+  const bool small = total <= 0x7fffffff;  // 32-bit index decode (64-bit division is ~5x dearer)
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    int fi = (int)(idx / hs);
-    int64_t r = idx - fi * hs;
-    int b2 = (int)(r % gd.Gh);
-    r /= gd.Gh;
-    int b1 = (int)(r % gd.G[1]);
-    int b0 = (int)(r / gd.G[1]);
+    int fi, b0, b1, b2;
+    if (small) {
+      const int id = (int)idx, h32 = (int)hs;
+      fi = id / h32;
+      int r = id - fi * h32;
+      b2 = r % gd.Gh;
+      r /= gd.Gh;
+      b1 = r % gd.G[1];
+      b0 = r / gd.G[1];
+    } else {
+      fi = (int)(idx / hs);
+      int64_t r = idx - fi * hs;
+      b2 = (int)(r % gd.Gh);
+      r /= gd.Gh;
+      b1 = (int)(r % gd.G[1]);
+      b0 = (int)(r / gd.G[1]);
+    }
     int s0[2], s1[2], s2[2];
     int n0 = bin_sources(b0, gd.G[0], gd.K[0], gd.B[0], s0);
     int n1 = bin_sources(b1, gd.G[1], gd.K[1], gd.B[1], s1);
@@ -271,14 +283,26 @@ __global__ void __launch_bounds__(256) k_gather(const Cx<T>* __restrict__ H, Gri
   const int64_t nb = (int64_t)gd.B[0] * gd.B[1] * gd.B[2];
   const int64_t hs = gd.half_size();
   const int64_t total = nb * nf;
+  const bool small = total <= 0x7fffffff;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    int fi = (int)(idx / nb);
-    int64_t r = idx - fi * nb;
-    int i2 = (int)(r % gd.B[2]);
-    r /= gd.B[2];
-    int i1 = (int)(r % gd.B[1]);
-    int i0 = (int)(r / gd.B[1]);
+    int fi, i0, i1, i2;
+    if (small) {
+      const int id = (int)idx, n32 = (int)nb;
+      fi = id / n32;
+      int r = id - fi * n32;
+      i2 = r % gd.B[2];
+      r /= gd.B[2];
+      i1 = r % gd.B[1];
+      i0 = r / gd.B[1];
+    } else {
+      fi = (int)(idx / nb);
+      int64_t r = idx - fi * nb;
+      i2 = (int)(r % gd.B[2]);
+      r /= gd.B[2];
+      i1 = (int)(r % gd.B[1]);
+      i0 = (int)(r / gd.B[1]);
+    }
     int f0 = freq_of(i0, gd.K[0], gd.B[0]), f1 = freq_of(i1, gd.K[1], gd.B[1]),
         f2 = freq_of(i2, gd.K[2], gd.B[2]);
     const C* Hf = H + fi * hs;
