@@ -7,6 +7,7 @@
 //          1/prod(G), applies the collision weights and symmetrizes.
 // Band-pointwise operators (Helmholtz, Leray, divergence) and the
 // deterministic two-pass reductions used by the solver also live here.
+#include <cstdint>
 #include "blr_internal.cuh"
 
 #include <cmath>
@@ -154,8 +155,27 @@ cufftHandle get_plan(blr_ctx* c, bool pad, int batch, bool forward) {
   return h;
 }
 
+// cuFFT wants 16-byte aligned real arrays; odd pad sizes put slices of the
+// D(u) / D(phi) caches (and their batch strides) at 8-byte offsets.
+template <typename T>
+static bool fft_real_aligned(const T* p, int batch, int64_t rs) {
+  return (reinterpret_cast<uintptr_t>(p) % 16) == 0 && (batch == 1 || (rs * sizeof(T)) % 16 == 0);
+}
+
 template <typename T>
 void exec_c2r(blr_ctx* c, bool pad, int batch, Cx<T>* in, T* out) {
+  const int64_t rs = c->g.grid(pad).real_size();
+  if (!fft_real_aligned(out, batch, rs)) {  // through an aligned temporary, one field at a time
+    T* tmp = nullptr;
+    BLR_CUDA(cudaMallocAsync((void**)&tmp, (size_t)rs * sizeof(T), c->stream));
+    const int64_t hs = c->g.grid(pad).half_size();
+    for (int b = 0; b < batch; ++b) {
+      exec_c2r<T>(c, pad, 1, in + b * hs, tmp);
+      BLR_CUDA(cudaMemcpyAsync(out + b * rs, tmp, rs * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+    }
+    BLR_CUDA(cudaFreeAsync(tmp, c->stream));
+    return;
+  }
   cufftHandle h = get_plan(c, pad, batch, false);
   BLR_FFT(cufftSetStream(h, c->stream));
   GridDesc gd = c->g.grid(pad);
@@ -170,6 +190,18 @@ void exec_c2r(blr_ctx* c, bool pad, int batch, Cx<T>* in, T* out) {
 
 template <typename T>
 void exec_r2c(blr_ctx* c, bool pad, int batch, T* in, Cx<T>* out) {
+  const int64_t rs = c->g.grid(pad).real_size();
+  if (!fft_real_aligned(in, batch, rs)) {
+    T* tmp = nullptr;
+    BLR_CUDA(cudaMallocAsync((void**)&tmp, (size_t)rs * sizeof(T), c->stream));
+    const int64_t hs = c->g.grid(pad).half_size();
+    for (int b = 0; b < batch; ++b) {
+      BLR_CUDA(cudaMemcpyAsync(tmp, in + b * rs, rs * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+      exec_r2c<T>(c, pad, 1, tmp, out + b * hs);
+    }
+    BLR_CUDA(cudaFreeAsync(tmp, c->stream));
+    return;
+  }
   cufftHandle h = get_plan(c, pad, batch, true);
   BLR_FFT(cufftSetStream(h, c->stream));
   GridDesc gd = c->g.grid(pad);
