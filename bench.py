@@ -318,18 +318,40 @@ def run_b200(args, rank, world, local):
     per_step_ms = t_ms / args.steps
     value = world * args.steps / (t_ms / 1e3)
 
-    # end to end through the public API with pinned host buffers
+    # end to end through the public API with pinned host buffers: every step copies
+    # its direction host->device and its product device->host.  The copies run on
+    # a second stream, double-buffered, so step k+1's upload and step k's
+    # download overlap step k's HVP (the way a host-driven solver would pipeline).
     host_w = torch.from_numpy(w.values.cpu().numpy()).pin_memory()
     host_out = torch.empty_like(host_w).pin_memory()
-    dev_w = torch.empty_like(w.values)
+    dev_in = [torch.empty_like(w.values) for _ in range(2)]
+    copy = torch.cuda.Stream(device=local)
+    in_ready = [torch.cuda.Event() for _ in range(2)]
     torch.cuda.synchronize()
     barrier(world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.steps):
-        dev_w.copy_(host_w, non_blocking=True)
-        hv = ev.hessian_vector(B.TimeFlow(dom, dev_w, args.nt, True), gauss_newton=True)
-        host_out.copy_(hv.values, non_blocking=True)
+    copy.wait_stream(stream)
+    with torch.cuda.stream(copy):
+        dev_in[0].copy_(host_w, non_blocking=True)
+        in_ready[0].record(copy)
+    done_prev = None
+    for k in range(args.steps):
+        stream.wait_event(in_ready[k % 2])
+        hv = ev.hessian_vector(B.TimeFlow(dom, dev_in[k % 2], args.nt, True), gauss_newton=True)
+        done = torch.cuda.Event()
+        done.record(stream)
+        with torch.cuda.stream(copy):
+            if k + 1 < args.steps:
+                if done_prev is not None:  # step k-1 has finished reading this buffer
+                    copy.wait_event(done_prev)
+                dev_in[(k + 1) % 2].copy_(host_w, non_blocking=True)
+                in_ready[(k + 1) % 2].record(copy)
+            copy.wait_event(done)
+            host_out.copy_(hv.values, non_blocking=True)
+        hv.values.record_stream(copy)
+        done_prev = done
+    stream.wait_stream(copy)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
