@@ -73,3 +73,29 @@ def test_objective_on_cufft_path(name, kind, padf):
     assert rel(np_(ev.gradient.values), g[f"{kind}_grad"]) < 1e-10
     assert rel(np_(ev.hessian_vector(w, gauss_newton=True).values), g[f"{kind}_hvp_gn"]) < 1e-10
     assert rel(np_(ev.hessian_vector(w, gauss_newton=False).values), g[f"{kind}_hvp_newton"]) < 1e-10
+
+
+@pytest.mark.parametrize("N,K,alt", [(136, 64, 198), (48, 20, 66), (40, 16, 54)])
+def test_engine_lengths_match_cufft(N, K, alt):
+    """The largest engine lengths (196 = 14x14, 64, 50) against the cuFFT path
+    at another exact pad: both are the exact truncated convolution, so energy,
+    gradient and GN / Newton HVPs agree to round-off (3-D, deformation)."""
+    import bench
+
+    res = {}
+    for pad in ("engine", alt):
+        dom = B.Domain((N,) * 3, (K,) * 3, alpha=0.02, **({} if pad == "engine" else {"pad": (alt,) * 3}))
+        if pad == "engine":
+            assert dom.pad[0] in ENGINE_PADS
+        r = np.random.default_rng(3)
+        I0, I1 = bench.band_image(dom, r), bench.band_image(dom, r)
+        v = B.TimeFlow(dom, bench.smooth_vector_block(dom, r, 0.5 / N, 2.0)[None], 4, True)
+        w = B.TimeFlow(dom, bench.smooth_vector_block(dom, r, 0.5 / N, 2.0)[None], 4, True)
+        obj = DeformationObjective(dom, I0, I1, ProblemConfig(sigma2=0.1, n_time_steps=4))
+        ev = obj.gradient(v)
+        res[pad] = (ev.energy, np_(ev.gradient.values), np_(ev.hessian_vector(w, True).values),
+                    np_(ev.hessian_vector(w, False).values))
+    a, b = res["engine"], res[alt]
+    assert a[0] == pytest.approx(b[0], rel=1e-12)
+    for x, y in zip(a[1:], b[1:]):
+        assert rel(x, y) < 1e-10
