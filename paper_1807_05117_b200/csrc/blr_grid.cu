@@ -24,6 +24,14 @@ static FullDesc full_desc(const Geom& g) {
 }
 
 __device__ inline void unravel(const FullDesc& fd, int64_t i, int* x) {
+  if (fd.nn <= 0x7fffffff) {  // 32-bit divisions (the 64-bit ones cost ~5x)
+    int j = (int)i;
+    x[2] = j % fd.N[2];
+    j /= fd.N[2];
+    x[1] = j % fd.N[1];
+    x[0] = j / fd.N[1];
+    return;
+  }
   x[2] = (int)(i % fd.N[2]);
   i /= fd.N[2];
   x[1] = (int)(i % fd.N[1]);
@@ -39,10 +47,12 @@ __device__ inline int64_t ravel(const FullDesc& fd, int x0, int x1, int x2) {
 template <typename T>
 __device__ inline void sample_coords(const FullDesc& fd, const T* disp, int64_t i, const int* x,
                                      double* c) {
-  for (int a = 0; a < 3; ++a) c[a] = 0.0;
-  for (int comp = 0; comp < fd.d; ++comp) {
-    int a = 3 - fd.d + comp;
-    c[a] = (double)x[a] + (double)disp[comp * fd.nn + i] * (double)fd.N[a];
+  // static axis loop (no dynamically indexed local arrays): axis a carries
+  // displacement component a - (3 - d) when that is >= 0
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const int comp = a - (3 - fd.d);
+    c[a] = comp >= 0 ? (double)x[a] + (double)disp[comp * fd.nn + i] * (double)fd.N[a] : 0.0;
   }
 }
 
@@ -99,6 +109,7 @@ __device__ inline double interp_at(const T* __restrict__ f, const FullDesc& fd, 
   // cubic on prefiltered coefficients
   int ib[3];
   double w[3][4];
+#pragma unroll
   for (int a = 0; a < 3; ++a) {
     double fl = floor(c[a]);
     ib[a] = (int)fl - 1;
@@ -109,14 +120,17 @@ __device__ inline double interp_at(const T* __restrict__ f, const FullDesc& fd, 
     }
   }
   double acc = 0.0;
+#pragma unroll
   for (int p = 0; p < 4; ++p) {
     if (w[0][p] == 0.0) continue;
     int x0 = pmod(ib[0] + p, fd.N[0]);
     double a1 = 0.0;
+#pragma unroll
     for (int q = 0; q < 4; ++q) {
       if (w[1][q] == 0.0) continue;
       int x1 = pmod(ib[1] + q, fd.N[1]);
       double a2 = 0.0;
+#pragma unroll
       for (int s = 0; s < 4; ++s) {
         int x2 = pmod(ib[2] + s, fd.N[2]);
         a2 += w[2][s] * (double)f[ravel(fd, x0, x1, x2)];
@@ -350,9 +364,13 @@ __global__ void __launch_bounds__(256) k_state_gn(const T* __restrict__ dlam, co
       T val = (T)interp_at<T>(dlam, fd, c, interp);
       T lam = vol[(int64_t)k * fd.nn + i] * val;
       T wk = (T)w.w[k];
-      for (int a = 0; a < fd.d; ++a) s[a] += wk * (lam * gm[((int64_t)k * fd.d + a) * fd.nn + i]);
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        if (a < fd.d) s[a] += wk * (lam * gm[((int64_t)k * fd.d + a) * fd.nn + i]);
     }
-    for (int a = 0; a < fd.d; ++a) acc[a * fd.nn + i] = add ? acc[a * fd.nn + i] + s[a] : s[a];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      if (a < fd.d) acc[a * fd.nn + i] = add ? acc[a * fd.nn + i] + s[a] : s[a];
   }
 }
 
