@@ -218,11 +218,11 @@ void exec_r2c(blr_ctx* c, bool pad, int batch, T* in, Cx<T>* out) {
 // scatter: band blocks -> half spectrum (zeros included), derivative fused
 // ---------------------------------------------------------------------------
 // Sources mapping to bin b on one axis (1 or 2 block indices, ascending).
-__device__ inline int bin_sources(int b, int G, int K, int B, int* src) {
-  int n = 0;
-  if (b <= K) src[n++] = b;
-  if (b >= G - K) src[n++] = b - G + B;  // frequency b - G in [-K, -1]
-  return n;
+__device__ inline int bin_sources(int b, int G, int K, int B, int& s0, int& s1) {
+  const bool lo = b <= K, hi = b >= G - K;  // frequency b - G in [-K, -1] for hi
+  s0 = lo ? b : b - G + B;
+  s1 = b - G + B;
+  return (lo ? 1 : 0) + (hi ? 1 : 0);
 }
 
 template <typename T>
@@ -251,27 +251,34 @@ __global__ void __launch_bounds__(256) k_scatter(ScatterArgs<T> a, GridDesc gd, 
       b0 = (int)(r / gd.G[1]);
     }
     int s0[2], s1[2], s2[2];
-    int n0 = bin_sources(b0, gd.G[0], gd.K[0], gd.B[0], s0);
-    int n1 = bin_sources(b1, gd.G[1], gd.K[1], gd.B[1], s1);
-    int n2 = bin_sources(b2, gd.G[2], gd.K[2], gd.B[2], s2);
+    int n0 = bin_sources(b0, gd.G[0], gd.K[0], gd.B[0], s0[0], s0[1]);
+    int n1 = bin_sources(b1, gd.G[1], gd.K[1], gd.B[1], s1[0], s1[1]);
+    int n2 = bin_sources(b2, gd.G[2], gd.K[2], gd.B[2], s2[0], s2[1]);
     C acc;
     acc.x = 0;
     acc.y = 0;
     const ScatterField<T>& F = a.f[fi];
-    for (int p = 0; p < n0; ++p)
-      for (int q = 0; q < n1; ++q)
-        for (int s = 0; s < n2; ++s) {
-          int i0 = s0[p], i1 = s1[q], i2 = s2[s];
+    // fixed-trip loops (<= 2 sources per axis) and scalar frequencies: no
+    // dynamically indexed local arrays
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          if (p >= n0 || q >= n1 || s >= n2) continue;
+          int i0 = p ? s0[1] : s0[0], i1 = q ? s1[1] : s1[0], i2 = s ? s2[1] : s2[0];
           int64_t off = ((int64_t)i0 * gd.B[1] + i1) * gd.B[2] + i2;
-          int fr[3] = {freq_of(i0, gd.K[0], gd.B[0]), freq_of(i1, gd.K[1], gd.B[1]),
-                       freq_of(i2, gd.K[2], gd.B[2])};
+          const int fr0 = freq_of(i0, gd.K[0], gd.B[0]), fr1 = freq_of(i1, gd.K[1], gd.B[1]),
+                    fr2 = freq_of(i2, gd.K[2], gd.B[2]);
           C val;
           val.x = 0;
           val.y = 0;
           for (int t = 0; t < F.nterms; ++t) {
             C z = F.src[t][off];
-            if (F.axis[t] >= 0) {
-              T k = (T)(kTwoPi * (double)fr[F.axis[t]]);
+            const int ax = F.axis[t];
+            if (ax >= 0) {
+              T k = (T)(kTwoPi * (double)(ax == 0 ? fr0 : (ax == 1 ? fr1 : fr2)));
               T re = -(k * z.y), im = k * z.x;  // (i k) * z
               z.x = re;
               z.y = im;
