@@ -376,10 +376,12 @@ void realize(blr_ctx* c, bool pad, const std::vector<ScatterField<T>>& fields, T
     int nterms = 0;
     for (int i = 0; i < nf; ++i) nterms += a.f[i].nterms;
     const double band_half = (double)gd.B[0] * gd.B[1] * (gd.K[2] + 1);
-    ProfScope ps(c, pad ? "scatter_pad" : "scatter_full",
-                 ((double)nf * hs + nterms * band_half) * sizeof(Cx<T>));
-    k_scatter<T><<<grid_blocks(hs * nf, 256), 256, 0, c->stream>>>(a, gd, H);
-    BLR_LAUNCHED();
+    {
+      ProfScope ps(c, pad ? "scatter_pad" : "scatter_full",
+                   ((double)nf * hs + nterms * band_half) * sizeof(Cx<T>));
+      k_scatter<T><<<grid_blocks(hs * nf, 256), 256, 0, c->stream>>>(a, gd, H);
+      BLR_LAUNCHED();
+    }
     exec_c2r<T>(c, pad, nf, H, out + off * rs);
     off += nf;
   }
