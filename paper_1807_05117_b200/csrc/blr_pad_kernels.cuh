@@ -1127,24 +1127,36 @@ __global__ void __launch_bounds__(kPWF * 32, 3) k_xfwd(FwdArgs<T> a, PadGeom g, 
     }
     if (t == nt - 1) {
       __syncthreads();
+      const Cx<T>* src = res;
+      T sc = a.scale;
       if (kz == 0) {
-        // symmetrize (kx, ky) with (-kx, -ky) inside the item, then the epilogue
-        epilogue_block<T, LPC>(a, O, o, g, [&](int ix, int sl, int64_t& e, Cx<T>& r) {
-          if (sl < LPW ? sl >= m.c1 : sl - LPW >= m.c2) return false;
+        // symmetrize (kx, ky) with (-kx, -ky) inside the item into the consumed
+        // slab, then the common epilogue
+        Cx<T>* sym = slab + b * SLAB;
+        for (int i = threadIdx.x; i < B0 * LPC; i += blockDim.x) {
+          const int ix = i / LPC, sl = i - (i / LPC) * LPC;
+          if (sl < LPW ? sl >= m.c1 : sl - LPW >= m.c2) continue;
           const int mix = ix == 0 ? 0 : B0 - ix;
           const Cx<T> p = res[ix * LPCS + sl], q = res[mix * LPCS + mirror_slot(m, sl)];
-          r = cx<T>((T)0.5 * a.scale * (p.x + q.x), (T)0.5 * a.scale * (p.y - q.y));
-          e = (int64_t)ix * B1 + slot_iy(m, sl);
-          return true;
-        });
-      } else {
-        epilogue_block<T, LPC>(a, O, o, g, [&](int ix, int l, int64_t& e, Cx<T>& r) {
-          if (l >= m.c1) return false;
-          e = ((int64_t)kz * B0 + ix) * B1 + m.cky0 + l;
-          r = cscale(res[ix * LPCS + l], a.scale);
-          return true;
-        });
+          sym[ix * LPCS + sl] = cx<T>((T)0.5 * a.scale * (p.x + q.x), (T)0.5 * a.scale * (p.y - q.y));
+        }
+        __syncthreads();
+        src = sym;
+        sc = (T)1;
       }
+      epilogue_block<T, LPC>(a, O, o, g, [&](int ix, int l, int64_t& e, Cx<T>& r) {
+        int iy;
+        if (kz > 0) {
+          if (l >= m.c1) return false;
+          iy = m.cky0 + l;
+        } else {
+          if (l < LPW ? l >= m.c1 : l - LPW >= m.c2) return false;
+          iy = slot_iy(m, l);
+        }
+        e = ((int64_t)kz * B0 + ix) * B1 + iy;
+        r = cscale(src[ix * LPCS + l], sc);
+        return true;
+      });
     }
     __syncthreads();
     it = nit;
