@@ -1340,7 +1340,10 @@ void launch_lines(blr_ctx* c, PadEngine* e, const LineArgs<T>& a) {
   if (sm > (size_t)e->line_smem_max) throw Error(1, "z-line kernel shared memory exceeds the device limit");
   static bool attr_done[2] = {false, false};
   if (!attr_done[sizeof(T) == 8 ? 0 : 1]) {
-    BLR_CUDA(cudaFuncSetAttribute(k_zlines<T, S, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, e->line_smem_max));
+    cudaFuncAttributes fa;
+    BLR_CUDA(cudaFuncGetAttributes(&fa, k_zlines<T, S, OP>));  // static shared memory counts too
+    BLR_CUDA(cudaFuncSetAttribute(k_zlines<T, S, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  e->line_smem_max - (int)fa.sharedSizeBytes));
     attr_done[sizeof(T) == 8 ? 0 : 1] = true;
   }
   constexpr int LPC = kZWarps * S::LPW;
