@@ -21,7 +21,13 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
-                "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+                "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills",
+                # the fp64 transforms are latency-bound: registers buy ILP (A/B: -0.7% HVP time)
+                "-Xptxas", "--register-usage-level=10"]
+# experiments: extra ptxas options, e.g. BLR_PTXAS="--register-usage-level=10"
+if os.environ.get("BLR_PTXAS"):
+    for _opt in os.environ["BLR_PTXAS"].split():
+        FLAGS += ["-Xptxas", _opt]
 
 
 def sources():
