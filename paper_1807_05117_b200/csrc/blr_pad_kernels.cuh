@@ -966,7 +966,7 @@ __device__ __forceinline__ void epilogue(const FwdArgs<T>& a, const FwdOut<T>& O
 template <typename T, int LPC, class Elem>
 __device__ __forceinline__ void epilogue_block(const FwdArgs<T>& a, const FwdOut<T>& O, int o, const PadGeom& g,
                                                Elem elem) {
-  constexpr int U = 2;
+  constexpr int U = 4;
   const int B0 = g.B[0];
   const int n = B0 * LPC;
   const int s = a.rk_s;
