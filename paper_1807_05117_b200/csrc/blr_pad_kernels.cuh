@@ -27,6 +27,7 @@
 #include <array>
 #include <cstring>
 #include <utility>
+#include <type_traits>
 
 namespace blr {
 
@@ -597,37 +598,62 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
       for (int n1 = 0; n1 < S::R1; ++n1) vreg[j][n1] = oka ? __ldg(vj + S::R2 * n1) : (T)0;
     }
   }
-  if constexpr (OP == kOpMapTC) {
-    // acc_i = sum_j Du_ij dV_j  (rin: Du [0,dd) V [dd,dd+d) dV [dd+d, dd+2d)); branch-free
-    // unrolled loads (absent components read component 0 and are masked)
-    if (own) {
+  // MapTC: acc_i += sum_j Du_ij dV_j (rin: Du [0,dd) V [dd,dd+d) dV [dd+d, dd+2d)).
+  // The k2 columns are split into five chunks, one per input pair: a chunk's
+  // loads are issued before that pair's transform and consumed after it, so
+  // the D(u) / dv reads overlap FFT work instead of stalling the kernel start.
+  // Absent components (d < 3) read component 0 and are masked.
+  constexpr int DCH = (S::R2 + 4) / 5;  // k2 columns per chunk
+  T dbuf[OP == kOpMapTC ? DCH : 1][12];
+  auto du_issue = [&](auto cc) {
+    constexpr int c = decltype(cc)::value;
+    if constexpr (OP == kOpMapTC) {
       const int d = a.d, dd = d * d;
-      const T* du[3][3];
-      const T* dv[3];
-      T msk[3];
+      const int64_t base = rline + (own ? bl : 0) * L + k1;
 #pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        const int jc = j < d ? j : 0;
-        msk[j] = j < d ? (T)1 : (T)0;
-        dv[j] = a.rin[dd + d + jc] + rline + bl * L + k1;
+      for (int u = 0; u < DCH; ++u) {
+        constexpr int dummy = 0;
+        (void)dummy;
+        const int k2 = c * DCH + u;
+        if (k2 >= S::R2) continue;
 #pragma unroll
-        for (int o = 0; o < 3; ++o) du[o][j] = a.rin[(o < d ? o : 0) * d + jc] + rline + bl * L + k1;
-      }
+        for (int j = 0; j < 3; ++j) {
+          const int jc = j < d ? j : 0;
+          dbuf[u][j] = __ldg(a.rin[dd + d + jc] + base + S::R1 * k2);
 #pragma unroll
-      for (int k2 = 0; k2 < S::R2; ++k2) {
-        T vj[3];
-#pragma unroll
-        for (int j = 0; j < 3; ++j) vj[j] = msk[j] * __ldg(dv[j] + S::R1 * k2);
-#pragma unroll
-        for (int o = 0; o < NOM; ++o) {
-          T s = 0;
-#pragma unroll
-          for (int j = 0; j < 3; ++j) s += __ldg(du[o < 3 ? o : 0][j] + S::R1 * k2) * vj[j];
-          acc[o][k2] = s;
+          for (int o = 0; o < 3; ++o) dbuf[u][3 + 3 * o + j] = __ldg(a.rin[(o < d ? o : 0) * d + jc] + base + S::R1 * k2);
         }
       }
     }
-  }
+  };
+  auto du_acc = [&](auto cc) {
+    constexpr int c = decltype(cc)::value;
+    if constexpr (OP == kOpMapTC) {
+      const int d = a.d;
+#pragma unroll
+      for (int u = 0; u < DCH; ++u) {
+        const int k2 = c * DCH + u;
+        if (k2 >= S::R2) continue;
+#pragma unroll
+        for (int o = 0; o < NOM; ++o) {
+          T sdu = 0;
+#pragma unroll
+          for (int j = 0; j < 3; ++j) sdu += (j < d ? dbuf[u][3 + 3 * (o < 3 ? o : 0) + j] : (T)0) * dbuf[u][j];
+          acc[o][k2] += sdu;
+        }
+      }
+    }
+  };
+  auto du_chunk = [&](int c, auto f) {
+    switch (c) {
+      case 0: f(std::integral_constant<int, 0>{}); break;
+      case 1: f(std::integral_constant<int, 1>{}); break;
+      case 2: f(std::integral_constant<int, 2>{}); break;
+      case 3: f(std::integral_constant<int, 3>{}); break;
+      case 4: f(std::integral_constant<int, 4>{}); break;
+      default: break;
+    }
+  };
   for (int q = 0; q < total; ++q) {
     if (q + 1 < total) {
       prefetch(q + 1);
@@ -683,7 +709,9 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
         for (int o = 0; o < NOM; ++o) acc[o][k2] += c1[o] * p1 + c2[o] * p2;
       }
     };
+    if constexpr (OP == kOpMapTC) du_chunk(q, du_issue);
     wfft<T, S, true>(tile, twp, nl, load, store);
+    if constexpr (OP == kOpMapTC) du_chunk(q, du_acc);
     if constexpr (OP == kOpContract) {
       if (p == npair - 1) {
         // node complete: rho_n is realized in Rsm.  Stream the cached D(phi_n)
@@ -726,6 +754,12 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
         }
         __syncwarp();
       }
+    }
+  }
+  if constexpr (OP == kOpMapTC) {
+    for (int c = total; c < 5; ++c) {  // fewer than five input pairs (d < 3)
+      du_chunk(c, du_issue);
+      du_chunk(c, du_acc);
     }
   }
   if constexpr (OP == kOpRealize) return;
