@@ -503,7 +503,8 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
                             sizeof(T) * (size_t)(nreal + nst) * S::LPW * L;
   // fp64: twiddles straight from the engine's global table (L1-resident), which
   // keeps the CTA's shared footprint at 6 CTAs per SM; fp32 converts into smem
-  constexpr bool kTwG = sizeof(T) == 8;
+  // register-bound ACC ops keep the twiddles in (otherwise unused) shared memory
+  constexpr bool kTwG = sizeof(T) == 8 && !(Tr::acc && OP != kOpContract);
   constexpr int kTwN = kTwG ? 0 : L;
   Cx<T>* tw = (Cx<T>*)smem_raw;
   const Cx<T>* twp = kTwG ? reinterpret_cast<const Cx<T>*>(twz_g) : tw;
@@ -1370,7 +1371,8 @@ void launch_lines(blr_ctx* c, PadEngine* e, const LineArgs<T>& a) {
   const size_t stage_n = std::max<size_t>(4 * (size_t)g.Kz1 * S::LPW + S::LPW, (size_t)S::LPW * S::L);
   const size_t warp_bytes = sizeof(Cx<T>) * ((size_t)S::TILE + stage_n) +
                             sizeof(T) * (size_t)(nreal + nst) * S::LPW * S::L;
-  const size_t sm = (sizeof(T) == 8 ? 0 : S::L * sizeof(Cx<T>)) + kZWarps * warp_bytes;
+  const bool twg = sizeof(T) == 8 && !(ZOp<OP>::acc && OP != kOpContract);  // as kTwG in the kernel
+  const size_t sm = (twg ? 0 : S::L * sizeof(Cx<T>)) + kZWarps * warp_bytes;
   if (sm > (size_t)e->line_smem_max) throw Error(1, "z-line kernel shared memory exceeds the device limit");
   static bool attr_done[2] = {false, false};
   if (!attr_done[sizeof(T) == 8 ? 0 : 1]) {
