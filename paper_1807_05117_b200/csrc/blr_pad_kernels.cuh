@@ -960,38 +960,6 @@ struct FwdArgs {
   Cx<T>* stage;
 };
 
-template <typename T>
-__device__ __forceinline__ void epilogue(const FwdArgs<T>& a, const FwdOut<T>& O, int64_t h, int64_t vidx, Cx<T> r) {
-  Cx<T> k;
-  if (O.mode == kEpiNegAdd) {
-    const Cx<T> v = O.vt[vidx];
-    k = cx<T>(-(v.x + r.x), -(v.y + r.y));
-  } else if (O.mode == kEpiNeg) {
-    k = cx<T>(-r.x, -r.y);
-  } else {
-    k = r;
-  }
-  if (a.kout) a.kout[h] = k;
-  if (a.rk_s) {
-    const Cx<T> cc = a.cur[h];
-    Cx<T> ac;
-    const int s = a.rk_s;
-    if (s == 1) {
-      ac = k;
-    } else {
-      ac = a.acc[h];
-      const T m = s < 4 ? (T)2 : (T)1;
-      ac = cx<T>(ac.x + m * k.x, ac.y + m * k.y);
-    }
-    if (s < 4) {
-      a.acc[h] = ac;
-      a.stage[h] = cx<T>(cc.x + a.cs * k.x, cc.y + a.cs * k.y);
-    } else {
-      a.cur[h] = cx<T>(cc.x + a.h6 * ac.x, cc.y + a.h6 * ac.y);
-    }
-  }
-}
-
 // Cooperative epilogue of one (output, kz, ky-chunk) block from the result
 // tile res[ix][LPCS]: consecutive threads take consecutive ky (coalesced), and
 // each thread issues the operand loads of U elements before any store, so the
