@@ -327,31 +327,40 @@ def run_b200(args, rank, world, local):
     dev_in = [torch.empty_like(w.values) for _ in range(2)]
     copy = torch.cuda.Stream(device=local)
     in_ready = [torch.cuda.Event() for _ in range(2)]
+
+    def pipelined(nsteps):
+        """nsteps HVPs through the public API, host in -> host out; returns the last product."""
+        copy.wait_stream(stream)
+        with torch.cuda.stream(copy):
+            dev_in[0].copy_(host_w, non_blocking=True)
+            in_ready[0].record(copy)
+        done_prev = hv = None
+        for k in range(nsteps):
+            stream.wait_event(in_ready[k % 2])
+            hv = ev.hessian_vector(B.TimeFlow(dom, dev_in[k % 2], args.nt, True), gauss_newton=True)
+            done = torch.cuda.Event()
+            done.record(stream)
+            with torch.cuda.stream(copy):
+                if k + 1 < nsteps:
+                    if done_prev is not None:  # step k-1 has finished reading this buffer
+                        copy.wait_event(done_prev)
+                    dev_in[(k + 1) % 2].copy_(host_w, non_blocking=True)
+                    in_ready[(k + 1) % 2].record(copy)
+                copy.wait_event(done)
+                host_out.copy_(hv.values, non_blocking=True)
+            hv.values.record_stream(copy)
+            done_prev = done
+        stream.wait_stream(copy)
+        return hv
+
+    # untimed warm-up of the pipelined loop: the allocator's growth under
+    # record_stream (product buffers held by the copy stream) is first-use set-up
+    hv = pipelined(max(args.warmup, 2))
     torch.cuda.synchronize()
     barrier(world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    copy.wait_stream(stream)
-    with torch.cuda.stream(copy):
-        dev_in[0].copy_(host_w, non_blocking=True)
-        in_ready[0].record(copy)
-    done_prev = None
-    for k in range(args.steps):
-        stream.wait_event(in_ready[k % 2])
-        hv = ev.hessian_vector(B.TimeFlow(dom, dev_in[k % 2], args.nt, True), gauss_newton=True)
-        done = torch.cuda.Event()
-        done.record(stream)
-        with torch.cuda.stream(copy):
-            if k + 1 < args.steps:
-                if done_prev is not None:  # step k-1 has finished reading this buffer
-                    copy.wait_event(done_prev)
-                dev_in[(k + 1) % 2].copy_(host_w, non_blocking=True)
-                in_ready[(k + 1) % 2].record(copy)
-            copy.wait_event(done)
-            host_out.copy_(hv.values, non_blocking=True)
-        hv.values.record_stream(copy)
-        done_prev = done
-    stream.wait_stream(copy)
+    hv = pipelined(args.steps)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)

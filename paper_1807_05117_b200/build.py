@@ -15,7 +15,9 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT_DIR = os.path.join(HERE, "_lib")
+# experiments: BLR_OUT_DIR builds a variant library elsewhere (e.g. _lib/var_u6),
+# loaded at run time through BLR_LIB_PATH (see _lib.py)
+OUT_DIR = os.environ.get("BLR_OUT_DIR") or os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libblreg_b200.so")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
@@ -28,6 +30,9 @@ FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
 if os.environ.get("BLR_PTXAS"):
     for _opt in os.environ["BLR_PTXAS"].split():
         FLAGS += ["-Xptxas", _opt]
+# experiments: compile-time tuning macros, e.g. BLR_DEFINES="BLR_EPI_U=6 BLR_KPW=2"
+if os.environ.get("BLR_DEFINES"):
+    FLAGS += [f"-D{_d}" for _d in os.environ["BLR_DEFINES"].split()]
 
 
 def sources():

@@ -190,7 +190,10 @@ struct Stager {
 // Staged pass kernels: kPW warps per CTA; the CTA's whole input slab is
 // copied to shared memory with coalesced cp.async first, then every warp runs
 // its four-step FFTs from shared memory.
-constexpr int kPW = 4;   // inverse passes (x, y)
+#ifndef BLR_KPW
+#define BLR_KPW 4
+#endif
+constexpr int kPW = BLR_KPW;  // inverse passes (x, y)
 constexpr int kPWF = 2;  // forward passes (y, x): measured best at 2 warps per CTA
 
 // Shared-memory strides chosen so the FFT access patterns are free of bank
@@ -969,7 +972,10 @@ struct FwdArgs {
 template <typename T, int LPC, class Elem>
 __device__ __forceinline__ void epilogue_block(const FwdArgs<T>& a, const FwdOut<T>& O, int o, const PadGeom& g,
                                                Elem elem) {
-  constexpr int U = 4;
+#ifndef BLR_EPI_U
+#define BLR_EPI_U 4
+#endif
+  constexpr int U = BLR_EPI_U;
   const int B0 = g.B[0];
   const int n = B0 * LPC;
   const int s = a.rk_s;
