@@ -262,6 +262,17 @@ constexpr int first_factor(int N) {
   return N % 4 == 0 ? 4 : N % 2 == 0 ? 2 : N % 3 == 0 ? 3 : N % 5 == 0 ? 5 : N % 7 == 0 ? 7 : N;
 }
 
+constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
+constexpr int inv_mod(int a, int m) {  // a^-1 mod m (gcd(a, m) = 1)
+  int r = 1;
+  while ((a * r) % m != 1 % m) ++r;
+  return r % m;
+}
+#ifndef BLR_PFA
+#define BLR_PFA 1
+#endif
+constexpr bool kPfa = BLR_PFA != 0;
+
 // in-register DFT of size N; INV selects exp(+2 pi i m r / N)
 template <typename T, int N, bool INV>
 __device__ __forceinline__ void dft(Cx<T>* v) {
@@ -317,6 +328,33 @@ __device__ __forceinline__ void dft(Cx<T>* v) {
     }
 #pragma unroll
     for (int r = 0; r < N; ++r) v[r] = out[r];
+  } else if constexpr (kPfa && cgcd(first_factor(N), N / first_factor(N)) == 1) {
+    // composite with coprime factors (10 = 2 x 5, 14 = 2 x 7, 20, 28): Good-Thomas
+    // prime-factor mapping, n = (B*n1 + A*n2) mod N, k = (k1*B*Binv + k2*A*Ainv) mod N.
+    // No twiddle multiplies between the sub-transforms; the index maps are
+    // compile-time (fully unrolled register indices), so they cost nothing.
+    constexpr int A = first_factor(N);
+    constexpr int B = N / A;
+    constexpr int Binv = inv_mod(B, A), Ainv = inv_mod(A, B);
+    Cx<T> t[N];
+#pragma unroll
+    for (int n2 = 0; n2 < B; ++n2) {
+      Cx<T> s[A];
+#pragma unroll
+      for (int n1 = 0; n1 < A; ++n1) s[n1] = v[(B * n1 + A * n2) % N];
+      dft<T, A, INV>(s);
+#pragma unroll
+      for (int k1 = 0; k1 < A; ++k1) t[k1 * B + n2] = s[k1];
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < A; ++k1) {
+      Cx<T> s[B];
+#pragma unroll
+      for (int n2 = 0; n2 < B; ++n2) s[n2] = t[k1 * B + n2];
+      dft<T, B, INV>(s);
+#pragma unroll
+      for (int k2 = 0; k2 < B; ++k2) v[(k1 * B * Binv + k2 * A * Ainv) % N] = s[k2];
+    }
   } else {
     // composite: four-step in registers, n = B*n1 + n2, k = k1 + A*k2
     constexpr int A = first_factor(N);
