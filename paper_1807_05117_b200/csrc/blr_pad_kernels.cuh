@@ -88,6 +88,13 @@ __device__ __forceinline__ void cp_async(Cx<T>* dst, const Cx<T>* src) {
 // kernel then hold SM resources through the predecessor's tail); the implicit
 // trigger at grid exit still removes the launch gap between kernels
 // (-1.1 ms per deformation GN HVP, the same as replaying a CUDA graph).
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+#ifndef BLR_XFWD_PF
+#define BLR_XFWD_PF 1
+#endif
+constexpr bool kXfwdPrefetch = BLR_XFWD_PF != 0;
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
@@ -1092,6 +1099,29 @@ __global__ void __launch_bounds__(kPWF * 32, 3) k_xfwd(FwdArgs<T> a, PadGeom g, 
         stg.rows(dst + LPW * LS, LS, base + (int64_t)slot_iy(m, LPW) * S::L, -(int64_t)S::L, m.c2, S::L, b);
     }
   };
+  // L1 prefetch of a kz > 0 item's epilogue operand rows (RK4 cur / acc and the
+  // kEpiNegAdd addend): each (kz, kx) row is c1 <= LPC consecutive ky, at most
+  // two 128-byte lines, so two prefetches per row and operand.  Issued when the
+  // item's first term starts, the lines land during its transforms instead of
+  // stalling the epilogue.  Rows are read only by this item (no staleness).
+  auto prefetch_epi = [&](int it_) {
+    if constexpr (kXfwdPrefetch) {
+      const int o = it_ / per;
+      const Item m = decode(it_ - o * per);
+      if (m.kz == 0) return;  // mirror items: scattered rows
+      const FwdOut<T>& O = a.o[o];
+      const int s = a.rk_s;
+      if (!s && O.mode != kEpiNegAdd) return;
+      for (int r = threadIdx.x; r < 2 * B0; r += blockDim.x) {
+        const int ix = r >> 1;
+        const int64_t e = ((int64_t)m.kz * B0 + ix) * B1 + m.cky0 + ((r & 1) ? m.c1 - 1 : 0);
+        const int64_t h = (int64_t)o * g.nh + e;
+        if (O.mode == kEpiNegAdd) prefetch_l1(O.vt + e);
+        if (s) prefetch_l1(a.cur + h);
+        if (s > 1) prefetch_l1(a.acc + h);
+      }
+    }
+  };
   load_tw<T>(tw, twg, S::L);
   int it = blockIdx.x, t = 0, b = 0;
   pdl_trigger();  // persistent grid: every CTA is already resident
@@ -1109,6 +1139,7 @@ __global__ void __launch_bounds__(kPWF * 32, 3) k_xfwd(FwdArgs<T> a, PadGeom g, 
     if (ntt >= nt) { nit = it + gridDim.x; ntt = 0; }
     if (nit < nitems) issue(nit, ntt, b ^ 1);
     stg.commit();
+    if (t == 0) prefetch_epi(it);
     stg.wait(b);
     const Item m = decode(it - o * per);
     const int kz = m.kz;
