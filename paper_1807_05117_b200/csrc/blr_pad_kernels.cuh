@@ -1034,7 +1034,10 @@ __device__ __forceinline__ void epilogue_block(const FwdArgs<T>& a, const FwdOut
 // Hermitian symmetrization of the kz = 0 plane (the reference's symmetrize)
 // happens inside the item: no separate fix-up kernel.
 template <typename T, class S>
-__global__ void __launch_bounds__(kPWF * 32, 3) k_xfwd(FwdArgs<T> a, PadGeom g, const double2* __restrict__ twg) {
+#ifndef BLR_XFWD_MINB
+#define BLR_XFWD_MINB 3
+#endif
+__global__ void __launch_bounds__(kPWF * 32, BLR_XFWD_MINB) k_xfwd(FwdArgs<T> a, PadGeom g, const double2* __restrict__ twg) {
   static_assert(kPWF == 2, "kz = 0 mirror items use one warp per half");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int LPW = S::LPW;
