@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--impl", choices=["b200", "reference", "selftest"], default="b200")
     ap.add_argument("--objective", choices=["deformation", "state"], default="deformation")
     ap.add_argument("--dtype", choices=["float64", "float32"], default="float64")
     ap.add_argument("--size", type=int, default=128)
@@ -72,16 +72,41 @@ def workload(args):
 # distributed plumbing
 # ---------------------------------------------------------------------------
 
-def dist_setup():
+_BACKEND = {"name": "nccl"}
+
+
+def free_port():
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn_ranks(nproc):
+    """``python bench.py --gpus N`` (N > 1) without torchrun: re-launch this
+    script under torch.distributed.run, one rank per GPU, and return its exit
+    code (the ranks print the JSON line)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def dist_setup(backend="nccl"):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    _BACKEND["name"] = backend
     if world > 1:
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return rank, world, local
 
 
@@ -92,15 +117,61 @@ def barrier(world):
         dist.barrier()
 
 
+def _dev():
+    return "cuda" if _BACKEND["name"] == "nccl" else "cpu"
+
+
 def max_over_ranks(x, world):
     if world == 1:
         return x
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_dev())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def rank_report(world, t_ms, e2e_ms, launches):
+    """Per-rank timings and evidence gathered over the communicator: device
+    ms of the timed region, e2e ms, kernel launches, whether this rank loaded
+    the in-tree sm_100a library, and the communicator size."""
+    import torch
+    import torch.distributed as dist
+
+    loaded = 0.0
+    try:
+        with open("/proc/self/maps") as f:
+            loaded = float("libblreg_b200.so" in f.read())
+    except OSError:
+        pass
+    mine = torch.tensor([float(dist.get_rank()), t_ms, e2e_ms, float(launches), loaded],
+                        dtype=torch.float64, device=_dev())
+    allv = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(allv, mine)
+    return {"backend": dist.get_backend(), "comm_size": dist.get_world_size(),
+            "per_rank": [{"rank": int(r[0]), "ms": round(float(r[1]), 3), "e2e_ms": round(float(r[2]), 3),
+                          "gpu_launches": int(r[3]), "native_lib_loaded": bool(r[4])}
+                         for r in (x.cpu() for x in allv)]}
+
+
+def run_selftest(args, rank, world):
+    """--impl selftest: the multi-rank plumbing (spawn, barrier, max over
+    ranks, per-rank gather) on gloo with a sleep standing in for the GPU step;
+    used by the CPU test suite."""
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        time.sleep(0.01 * (1 + rank))
+    local_ms = 1e3 * (time.perf_counter() - t0)
+    t_ms = max_over_ranks(local_ms, world)
+    line = {"metric": "selftest", "value": world * args.steps / (t_ms / 1e3), "unit": "steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
+            "impl": "selftest"}
+    if world > 1:
+        line["ranks"] = rank_report(world, local_ms, local_ms, 0)
+    if rank == 0:
+        print(json.dumps(line))
 
 
 # ---------------------------------------------------------------------------
@@ -313,8 +384,8 @@ def run_b200(args, rank, world, local):
         torch.cuda.synchronize()
     launches = (_lib.launch_count() - l0)
     barrier(world)
-    t_ms = start.elapsed_time(end)
-    t_ms = max_over_ranks(t_ms, world)
+    local_ms = start.elapsed_time(end)
+    t_ms = max_over_ranks(local_ms, world)
     per_step_ms = t_ms / args.steps
     value = world * args.steps / (t_ms / 1e3)
 
@@ -363,7 +434,8 @@ def run_b200(args, rank, world, local):
     hv = pipelined(args.steps)
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
+    local_e2e_ms = e0.elapsed_time(e1)
+    e2e_ms = max_over_ranks(local_e2e_ms, world)
     e2e_value = world * args.steps / (e2e_ms / 1e3)
     assert torch.equal(host_out, out.values.cpu()), "e2e result differs from the device-resident run"
 
@@ -438,8 +510,14 @@ def run_b200(args, rank, world, local):
     }
     if reg:
         line["registration"] = reg
+    if world > 1:
+        line["ranks"] = rank_report(world, local_ms, local_e2e_ms, launches)
     if rank == 0 and world == 1 and args.cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args, sample="one")
+        cpu = cpu_baseline(args, dom.pad, reg)
+        if "registration" in cpu:
+            reg["cpu_s_estimate"] = cpu["registration"]["cpu_s_estimate"]
+            reg["cpu_ratio"] = cpu["registration"]["ratio"]
+        line["cpu_baseline"] = cpu
     if rank == 0:
         print(json.dumps(line))
 
@@ -448,57 +526,125 @@ def run_b200(args, rank, world, local):
 # CPU baseline / reference arm (oracle port on the host cores)
 # ---------------------------------------------------------------------------
 
-def cpu_hvp_sample(args):
-    """Time the pieces of one GN HVP of the reference algorithm on the host
-    (oracle port, scipy.fft on all host threads) and scale to a whole HVP:
-    forward tangent stage x 4*Nt (+ momentum stage x 4*Nt + 11 node
-    contractions for the deformation objective).  Returns (seconds_per_hvp,
-    sample_seconds, description)."""
+def _oracle():
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import blreg_oracle as O
 
-    O.WORKERS = os.cpu_count() or 1
+    return O
+
+
+class HostThreads:
+    """Run the port on ``n`` host threads: scipy.fft workers = n and, for n = 1,
+    the process pinned to one core (``taskset`` equivalent); restored on exit."""
+
+    def __init__(self, O, n):
+        self.O, self.n = O, n
+
+    def __enter__(self):
+        self.prev_workers = self.O.WORKERS
+        self.O.WORKERS = self.n
+        self.prev_aff = os.sched_getaffinity(0)
+        if self.n == 1:
+            os.sched_setaffinity(0, {min(self.prev_aff)})
+        return self
+
+    def __exit__(self, *exc):
+        self.O.WORKERS = self.prev_workers
+        os.sched_setaffinity(0, self.prev_aff)
+
+
+def host_cores():
+    return len(os.sched_getaffinity(0))
+
+
+def port_problem(args, pad):
+    """The §8(d) micro-benchmark problem in the oracle port at ``pad`` (the
+    same inputs as the B200 arm, generated by the same seeded recipe)."""
+    O = _oracle()
     n, k, nt = args.size, args.band, args.nt
-    dom = O.Dom((n,) * 3, (k,) * 3, alpha=0.02, order=2)
+    dom = O.Dom((n,) * 3, (k,) * 3, alpha=0.02, order=2, pad=tuple(pad))
     rng = np.random.default_rng(0)
-    u = O.smooth_vector_block(dom, rng, 0.5 / n, 2.0)
-    du = O.smooth_vector_block(dom, rng, 0.5 / n, 2.0)
-    v = O.smooth_vector_block(dom, rng, 0.5 / n, 2.0)
-    dv = O.smooth_vector_block(dom, rng, 0.5 / n, 2.0)
+    I0, I1 = O.band_image(dom, rng), O.band_image(dom, rng)
+    v = O.Flow(dom, O.smooth_vector_block(dom, rng, 0.5 / n, decay=2.0)[None], nt, True)
+    w = O.Flow(dom, O.smooth_vector_block(dom, rng, 0.5 / n, decay=2.0)[None], nt, True)
+    kind = "def" if args.objective == "deformation" else "state"
+    obj = O.OracleObjective(dom, I0, I1, O.Problem(sigma2=0.1, n_time_steps=nt), kind=kind)
+    return O, dom, obj, v, w
+
+
+def _timed(fn):
     t0 = time.perf_counter()
-    O.rhs_map(dom, u, v)
-    O.rhs_map_tangent(dom, u, du, v, dv)
-    t_fwd = time.perf_counter() - t0
+    out = fn()
+    return out, time.perf_counter() - t0
+
+
+def cpu_stage_sample(args, pad):
+    """One forward-tangent RK4 stage (+ one momentum stage and one node
+    contraction for the deformation objective) of the port, and the count of
+    each per GN HVP.  Used only for the 1-core figure, which is an estimate."""
+    O = _oracle()
+    n, k, nt = args.size, args.band, args.nt
+    dom = O.Dom((n,) * 3, (k,) * 3, alpha=0.02, order=2, pad=tuple(pad))
+    rng = np.random.default_rng(0)
+    u, du, v, dv = (O.smooth_vector_block(dom, rng, 0.5 / n, 2.0) for _ in range(4))
     stages = 4 * nt
-    total = stages * t_fwd
-    desc = f"1 forward-tangent RK4 stage (rhs_map + rhs_map_tangent) x{stages}"
+    _, t_fwd = _timed(lambda: (O.rhs_map(dom, u, v), O.rhs_map_tangent(dom, u, du, v, dv)))
+    total, sample = stages * t_fwd, t_fwd
+    desc = f"1 forward-tangent RK4 stage x{stages}"
     if args.objective == "deformation":
-        t0 = time.perf_counter()
-        O.rhs_momentum_pair(dom, u, du, v, None)
-        t_mom = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        O.conv_matvec(dom, O.jac(dom, u), du, transpose=True)
-        t_con = time.perf_counter() - t0
+        _, t_mom = _timed(lambda: O.rhs_momentum_pair(dom, u, du, v, None))
+        _, t_con = _timed(lambda: O.conv_matvec(dom, O.jac(dom, u), du, transpose=True))
         total += stages * t_mom + (nt + 1) * t_con
-        desc += f" + 1 momentum-pair stage x{stages} + 1 node contraction x{nt + 1}"
-        sample = t_fwd + t_mom + t_con
-    else:
-        t0 = time.perf_counter()
-        img = np.random.default_rng(1).random(dom.shape)
-        disp = O.include(dom, u, check=False)
-        O.warp(dom, img, disp)
-        t_w = time.perf_counter() - t0
-        total += (nt + 1) * t_w
-        desc += f" + 1 node warp x{nt + 1}"
-        sample = t_fwd + t_w
-    return total, sample, desc + f" at {n}^3/K={k}, pad {dom.pad_shape[0]} (reference pad)"
+        sample += t_mom + t_con
+        desc += f" + 1 momentum stage x{stages} + 1 node contraction x{nt + 1}"
+    return total, sample, desc
 
 
-def cpu_baseline(args, sample="one"):
-    total, sample_s, desc = cpu_hvp_sample(args)
-    return {"value": 1.0 / total, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
-            "sample": desc, "sample_seconds": round(sample_s, 2),
-            "seconds_per_hvp_estimated": round(total, 2)}
+def cpu_baseline(args, pad, reg=None):
+    """SURVEY §8(d) CPU rows, measured on this host in this session:
+
+    * all cores: one WHOLE energy, gradient and GN HVP of the port (timed, not
+      scaled), at the B200 arm's exact pad;
+    * one core (pinned, 1 FFT worker): a stage sample scaled to one HVP
+      (labelled an estimate; a whole 1-core HVP takes minutes);
+    * CPU s/registration estimate t_CPU = sum over the B200 registration's
+      calls of substeps x t_op (transport cost is linear in substeps)."""
+    O, dom, obj, v, w = port_problem(args, pad)
+    cores = host_cores()
+    with HostThreads(O, cores):
+        _, t_energy = _timed(lambda: obj.energy(v))
+        ev, t_grad = _timed(lambda: obj.gradient(v))
+        _, t_hvp = _timed(lambda: obj.hessian_vector(ev, w, gauss_newton=True))
+    del ev
+    with HostThreads(O, 1):
+        t1, t1_sample, desc1 = cpu_stage_sample(args, pad)
+    out = {"value": 1.0 / t_hvp, "unit": UNIT, "cores": cores, "kind": "port",
+           "sample": f"1 whole {args.objective} GN HVP of the oracle port at {args.size}^3/K={args.band}/"
+                     f"Nt={args.nt}, pad {pad[0]} (= the B200 arm's pad; the reference's own pad "
+                     f"132 has 2.3x more points, so this baseline is conservative), scipy.fft on "
+                     f"{cores} threads, after one untimed gradient (the HVP's evaluation point)",
+           "seconds_per_hvp": round(t_hvp, 3),
+           "per_op_s": {"energy": round(t_energy, 3), "gradient": round(t_grad, 3),
+                        "hvp_gn": round(t_hvp, 3)},
+           "one_core": {"value": 1.0 / t1, "unit": UNIT, "cores": 1, "estimated": True,
+                        "seconds_per_hvp_estimated": round(t1, 2), "sample_seconds": round(t1_sample, 2),
+                        "sample": desc1 + " (process pinned to one core, 1 FFT worker)"}}
+    if reg and reg.get("calls"):
+        calls = reg["calls"]
+
+        def cost(name, t_op):
+            sub = calls.get(f"{name}_substeps")
+            n = calls.get(name, 0)
+            mean_sub = sub["mean_substeps"] if isinstance(sub, dict) and sub.get("n") else 1.0
+            return n * mean_sub * t_op
+
+        t_cpu = (cost("gradient", t_grad) + cost("hvp", t_hvp) + cost("energy", t_energy))
+        out["registration"] = {
+            "cpu_s_estimate": round(t_cpu, 2), "gpu_s": reg["s_per_registration"],
+            "ratio": round(t_cpu / reg["s_per_registration"], 1), "north_star_ratio": 50.0,
+            "formula": "sum over the B200 run's calls (gradient, hvp, energy) of n x mean substeps x "
+                       "the all-core per-op time above"}
+    return out
 
 
 def run_batch(args, rank, world, local):
@@ -548,40 +694,65 @@ def run_batch(args, rank, world, local):
 
 
 def run_reference(args, rank, world):
+    """The reference algorithm on the host CPU: the oracle port (numpy +
+    scipy.fft on every host thread) at the B200 arm's exact pad.  One step =
+    one WHOLE GN HVP, timed; the evaluation point (one gradient) is untimed
+    set-up.  Warm-up: min(W, 1) HVP (CPU code has no first-use costs beyond
+    scipy's FFT plan cache).  Under torchrun only rank 0 runs."""
     if rank != 0:
         return
-    for _ in range(args.warmup):
-        cpu_hvp_sample(args)
-    per = []
-    t0 = time.perf_counter()
-    desc = ""
-    for _ in range(args.steps):
-        total, _, desc = cpu_hvp_sample(args)
-        per.append(total)
-    wall = time.perf_counter() - t0
-    value = 1.0 / float(np.mean(per))
+    sys.path.insert(0, ROOT)
+    from paper_1807_05117_b200.domain import default_pad
+
+    pad = default_pad((args.band,) * 3)
+    O, dom, obj, v, w = port_problem(args, pad)
+    cores = host_cores()
+    t_all0 = time.perf_counter()
+    with HostThreads(O, cores):
+        ev, t_grad = _timed(lambda: obj.gradient(v))
+        for _ in range(min(args.warmup, 1)):
+            obj.hessian_vector(ev, w, gauss_newton=True)
+        per = []
+        for _ in range(args.steps):
+            _, t = _timed(lambda: obj.hessian_vector(ev, w, gauss_newton=True))
+            per.append(t)
+    wall = time.perf_counter() - t_all0
+    total = float(np.sum(per))
+    value = args.steps / total
+    desc = (f"whole {args.objective} GN HVPs of the oracle port at {args.size}^3/K={args.band}/"
+            f"Nt={args.nt}, pad {pad[0]}, scipy.fft on {cores} threads; {args.steps} timed HVPs")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(per)), "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (SURVEY §8(d) recipe, seed 0)", "impl": "reference",
-            "config": {**workload(args), "parallelism": "host CPU"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count() or 1,
-                             "kind": "port", "sample": desc},
+            "data": "synthetic (band_image pair + smooth v, w; SURVEY §8(d) recipe, seed 0)",
+            "impl": "reference",
+            "config": {**workload(args), "pad": list(pad), "parallelism": f"host CPU, {cores} threads"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": desc},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "wall_s": wall}
+            "per_step_s": [round(t, 3) for t in per], "setup_gradient_s": round(t_grad, 3),
+            "warmup_hvps": min(args.warmup, 1), "wall_s": round(wall, 2)}
     print(json.dumps(line))
 
 
 def main():
     args = parse()
+    world_env = os.environ.get("WORLD_SIZE")
+    if args.gpus > 1 and world_env is None:
+        sys.exit(spawn_ranks(args.gpus))
+    if world_env is not None and int(world_env) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}; "
+                         "launch with --gpus equal to the number of ranks")
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
         world = int(os.environ.get("WORLD_SIZE", "1"))
         run_reference(args, rank, world)
         return
-    rank, world, local = dist_setup()
+    rank, world, local = dist_setup("gloo" if args.impl == "selftest" else "nccl")
     try:
-        if args.batch:
+        if args.impl == "selftest":
+            run_selftest(args, rank, world)
+        elif args.batch:
             run_batch(args, rank, world, local)
         else:
             run_b200(args, rank, world, local)

@@ -38,9 +38,9 @@ typedef struct blr_ctx blr_ctx;
 /* ---- context ------------------------------------------------------------ */
 
 /* Domain + pad grid + metric.  Replaces Domain (domain.py:19-97) and the pad
- * choice _pad_shape (spectral.py:239-242; any pad >= 3K+1 is exact).
+ * choice _pad_shape (spectral.py:142-145; any pad >= 3K+1 is exact).
  * symbol_tab: per axis, B_a doubles of alpha-free symbol terms s_a(k)
- * (spectral.py:339-354: 2 N^2 (1 - cos(2 pi k / N)) or (2 pi k)^2),
+ * (spectral.py:242-257: 2 N^2 (1 - cos(2 pi k / N)) or (2 pi k)^2),
  * concatenated over the d axes. */
 int blr_ctx_create(blr_ctx** out, int ndim, const int* shape, const int* bandwidth,
                    const int* pad, double alpha, int order, const double* symbol_tab,
@@ -68,13 +68,13 @@ int blr_include(blr_ctx* ctx, int grid, const void* blocks, int nfields, const i
 /* project: real grid fields -> band blocks (forward DFT / prod, truncate,
  * symmetrize; spectral.py:122-135). */
 int blr_project(blr_ctx* ctx, int grid, const void* fields, int nfields, void* out);
-/* out = in * A(k)^power, power in {+order, -order} via sign (spectral.py:357-369) */
+/* out = in * A(k)^power, power in {+order, -order} via sign (spectral.py:260-272) */
 int blr_helmholtz(blr_ctx* ctx, const void* in, int nblocks, int inverse, void* out);
-/* Leray projection of vector blocks (spectral.py:400-425) */
+/* Leray projection of vector blocks (spectral.py:312-328) */
 int blr_leray(blr_ctx* ctx, const void* in, int nvec, void* out);
-/* spectral divergence of vector blocks (spectral.py:381-386), per vector */
+/* spectral divergence of vector blocks (spectral.py:284-289), per vector */
 int blr_divergence(blr_ctx* ctx, const void* in, int nvec, void* out);
-/* out = symmetrize(in) (spectral.py:142-144) */
+/* out = symmetrize(in) (spectral.py:45-47) */
 int blr_symmetrize(blr_ctx* ctx, const void* in, int nblocks, void* out);
 
 /* ---- linear algebra on flows (solver.py:88-126, transport.py:147-153) ----- */
@@ -142,7 +142,7 @@ int blr_momentum_contract(blr_ctx* ctx, const void* v, int n_stored, int n_steps
                           const void* rho_end, const void* phi_nodes, const double* weights,
                           int transpose, void* dphi_cache, int cache_mode, void* out);
 /* generic truncated product pi(iota(M) . iota(x)) with optional transpose
- * (spectral.conv_matvec, spectral.py:291-297) for one (d x d, d) pair. */
+ * (spectral.conv_matvec, spectral.py:194-200) for one (d x d, d) pair. */
 int blr_conv_matvec(blr_ctx* ctx, const void* M, const void* x, int transpose, void* out);
 
 /* ---- full-grid operations (gridops.py) ----------------------------------- */

@@ -87,7 +87,7 @@ class Dom:
         return float(np.prod(self.h))
 
     @property
-    def pad_shape(self):  # spectral.py:239-242
+    def pad_shape(self):  # spectral.py:142-145
         if self.pad is not None:
             return self.pad
         return tuple(scipy.fft.next_fast_len(2 * (b - 1) + 1) for b in self.block)
@@ -212,16 +212,16 @@ def project(dom: Dom, f: np.ndarray, grid=None) -> np.ndarray:
     return np.ascontiguousarray(out.reshape(lead + dom.block))
 
 
-def to_pad(dom, c):  # spectral.py:245-246
+def to_pad(dom, c):  # spectral.py:148-149
     return include(dom, c, dom.pad_shape, check=False)
 
 
-def from_pad(dom, f):  # spectral.py:249-250
+def from_pad(dom, f):  # spectral.py:152-153
     return project(dom, f, dom.pad_shape)
 
 
 # ---------------------------------------------------------------------------
-# diagonal operators (spectral.py:321-328, 339-425)
+# diagonal operators (spectral.py:242-328, 339-425)
 # ---------------------------------------------------------------------------
 
 def kvecs(dom):
@@ -230,7 +230,7 @@ def kvecs(dom):
 
 
 def base_symbol(dom):
-    """1 + alpha * sum_j s_j(k) (spectral.py:339-354)."""
+    """1 + alpha * sum_j s_j(k) (spectral.py:242-257)."""
     acc = np.zeros(dom.block)
     for ax, (m, n) in enumerate(zip(dom.block, dom.shape)):
         f = freqs_of(m)
@@ -242,31 +242,31 @@ def base_symbol(dom):
     return 1.0 + dom.alpha * acc
 
 
-def helmholtz(dom, c):  # spectral.py:357-364
+def helmholtz(dom, c):  # spectral.py:265-267
     return c * (base_symbol(dom) ** dom.order)
 
 
-def inv_helmholtz(dom, c):  # spectral.py:367-369
+def inv_helmholtz(dom, c):  # spectral.py:270-272
     return c * (base_symbol(dom) ** (-dom.order))
 
 
-def grad(dom, s):  # spectral.py:372-378
+def grad(dom, s):  # spectral.py:275-281
     return np.stack([1j * k * s for k in kvecs(dom)])
 
 
-def div(dom, v):  # spectral.py:381-386
+def div(dom, v):  # spectral.py:284-289
     out = np.zeros(dom.block, dtype=np.complex128)
     for ax, k in enumerate(kvecs(dom)):
         out += 1j * k * v[ax]
     return out
 
 
-def jac(dom, v):  # spectral.py:389-397 ; out[i, j] = d_j v_i
+def jac(dom, v):  # spectral.py:292-300 ; out[i, j] = d_j v_i
     ks = kvecs(dom)
     return np.stack([np.stack([1j * ks[j] * v[i] for j in range(dom.ndim)]) for i in range(dom.ndim)])
 
 
-def leray(dom, v):  # spectral.py:400-425
+def leray(dom, v):  # spectral.py:312-328
     dv = div(dom, v)
     lap = np.zeros(dom.block)
     for k in kvecs(dom):
@@ -277,19 +277,19 @@ def leray(dom, v):  # spectral.py:400-425
     return v - grad(dom, p)
 
 
-def inner(a, b):  # spectral.py:432-434
+def inner(a, b):  # spectral.py:335-337
     return float(np.real(np.vdot(b, a)))
 
 
-def grid_norm2(dom, f):  # spectral.py:441-442
+def grid_norm2(dom, f):  # spectral.py:344-345
     return dom.cell * float(np.sum(f * f))
 
 
-def max_abs(dom, c):  # spectral.py:445-447
+def max_abs(dom, c):  # spectral.py:348-350
     return float(np.max(np.abs(include(dom, c, check=False))))
 
 
-def conv_matvec(dom, M, v, transpose=False):  # spectral.py:291-297
+def conv_matvec(dom, M, v, transpose=False):  # spectral.py:194-200
     d = dom.ndim
     mg = to_pad(dom, M.reshape((d * d,) + dom.block)).reshape((d, d) + dom.pad_shape)
     vg = to_pad(dom, v)
@@ -297,7 +297,7 @@ def conv_matvec(dom, M, v, transpose=False):  # spectral.py:291-297
     return from_pad(dom, np.einsum(spec, mg, vg))
 
 
-def conv_scalar(dom, a, b):  # spectral.py:278-281
+def conv_scalar(dom, a, b):  # spectral.py:181-184
     return from_pad(dom, to_pad(dom, a) * to_pad(dom, b))
 
 

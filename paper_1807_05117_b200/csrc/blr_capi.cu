@@ -31,8 +31,23 @@ static void need(bool ok, const char* msg) {
   if (!ok) throw Error(1, msg);
 }
 
+// Makes the context's device current for the duration of one entry point and
+// restores the caller's device afterwards (a Domain on device k works without
+// the caller having called cudaSetDevice(k)).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) BLR_CUDA(cudaSetDevice(dev));
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 #define DISPATCH(ctx, ...)                  \
   do {                                      \
+    DeviceGuard dev_guard_((ctx)->device);  \
     if ((ctx)->dtype == 0) {                \
       using T = double;                     \
       __VA_ARGS__;                          \
@@ -99,7 +114,7 @@ int blr_ctx_create(blr_ctx** out, int ndim, const int* shape, const int* bandwid
       }
       dst += g.B[a];
     }
-    BLR_CUDA(cudaSetDevice(device));
+    DeviceGuard dev_guard(device);
     BLR_CUDA(cudaMalloc(&c->d_sym, nsym * sizeof(double)));
     BLR_CUDA(cudaMemcpy(c->d_sym, c->h_sym.data(), nsym * sizeof(double), cudaMemcpyHostToDevice));
     // keep stream-ordered temporaries cached across calls
@@ -114,6 +129,7 @@ int blr_ctx_create(blr_ctx** out, int ndim, const int* shape, const int* bandwid
 int blr_ctx_destroy(blr_ctx* c) {
   return guarded([&] {
     if (!c) return;
+    DeviceGuard dev_guard(c->device);
     cudaStreamSynchronize(c->stream);
     pad_engine_release(c);
     for (auto& kv : c->plans) cufftDestroy(kv.second);

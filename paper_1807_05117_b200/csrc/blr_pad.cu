@@ -6,6 +6,7 @@
 #include <array>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 
 namespace blr {
 
@@ -35,12 +36,19 @@ BLR_FOR_EACH_LZ(BLR_EXTERN_L_ALLOPS)
 // host side: engine setup and launch helpers
 // ---------------------------------------------------------------------------
 
+// Engine registry, one entry per context.  Entries are node-stable (std::map),
+// so a returned PadEngine* stays valid while other threads insert; the mutex
+// guards the map itself and each engine's one-time set-up.  Each context is
+// used by a single (thread, stream) pair (domain.py Context), so an engine's
+// scratch is never shared across threads or streams.
+static std::mutex g_engines_mu;
 static std::map<blr_ctx*, PadEngine>& engines() {
   static std::map<blr_ctx*, PadEngine> m;
   return m;
 }
 
 void pad_engine_release(blr_ctx* c) {
+  std::lock_guard<std::mutex> lk(g_engines_mu);
   auto it = engines().find(c);
   if (it == engines().end()) return;
   for (auto* p : it->second.tw)
@@ -54,6 +62,7 @@ static int g_pad_disabled = -1;
 
 template <typename T>
 static PadEngine* engine(blr_ctx* c) {
+  std::lock_guard<std::mutex> lk(g_engines_mu);
   PadEngine& e = engines()[c];
   if (e.tried) return e.ok ? &e : nullptr;
   e.tried = true;

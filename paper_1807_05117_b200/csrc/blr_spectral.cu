@@ -455,7 +455,7 @@ __device__ inline void band_freqs(const BandDesc& bd, int64_t r, int* f) {
   f[2] = freq_of(i2, bd.K[2], bd.B[2]);
 }
 
-// symbol A(k) = 1 + alpha * (t0[i0] + t1[i1] + t2[i2])  (spectral.py:339-354)
+// symbol A(k) = 1 + alpha * (t0[i0] + t1[i1] + t2[i2])  (spectral.py:242-257)
 __device__ inline double symbol_at(const double* sym, const BandDesc& bd, int64_t r, double alpha) {
   int i2 = (int)(r % bd.B[2]);
   r /= bd.B[2];
@@ -486,7 +486,7 @@ __global__ void k_helmholtz(const Cx<T>* in, int nblocks, BandDesc bd, const dou
   }
 }
 
-// Leray projection w = v - grad(lap^-1 div v), p(0) = 0 (spectral.py:400-425).
+// Leray projection w = v - grad(lap^-1 div v), p(0) = 0 (spectral.py:312-328).
 template <typename T>
 __global__ void k_leray(const Cx<T>* in, int nvec, int d, BandDesc bd, Cx<T>* out) {
   int64_t total = bd.nb * nvec;
@@ -761,8 +761,11 @@ __device__ inline double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
+// NaN-propagating max (np.max semantics: a NaN anywhere makes the result NaN;
+// fmax would drop it and let a NaN gradient read as converged).
+__device__ inline double nan_max(double a, double b) { return (a > b || a != a) ? a : b; }
 __device__ inline double warp_max(double v) {
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  for (int o = 16; o > 0; o >>= 1) v = nan_max(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
 
@@ -792,7 +795,7 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce(const void* pa, const vo
       Cx<T> a = ((const Cx<T>*)pa)[i], b = ((const Cx<T>*)pb)[i];
       acc += (double)a.x * (double)b.x + (double)a.y * (double)b.y;
     } else if (MODE == 1) {
-      acc = fmax(acc, fabs((double)((const T*)pa)[i]));
+      acc = nan_max(acc, fabs((double)((const T*)pa)[i]));
     } else if (MODE == 2) {
       double x = (double)((const T*)pa)[i];
       if (pb) x -= (double)((const T*)pb)[i];
@@ -809,7 +812,7 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce(const void* pa, const vo
 template <int OP>
 __global__ void k_reduce_final(const double* partial, int n, double* out) {
   double acc = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) acc = OP == 0 ? acc + partial[i] : fmax(acc, partial[i]);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc = OP == 0 ? acc + partial[i] : nan_max(acc, partial[i]);
   acc = block_reduce<OP>(acc);
   if (threadIdx.x == 0) out[0] = acc;
 }

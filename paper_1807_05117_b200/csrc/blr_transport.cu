@@ -280,7 +280,7 @@ static void set_unit_scalar(blr_ctx* c, Cx<T>* blk) {
   BLR_CUDA(cudaMemcpyAsync(blk, &one, sizeof(one), cudaMemcpyHostToDevice, c->stream));
 }
 
-// D(u) fields, out[i*d+j] = d_j u_i  (spectral_jacobian, spectral.py:389-397)
+// D(u) fields, out[i*d+j] = d_j u_i  (spectral_jacobian, spectral.py:292-300)
 template <typename T>
 static void push_jac(const Geom& g, const Cx<T>* u, std::vector<ScatterField<T>>& f) {
   for (int i = 0; i < g.d; ++i)

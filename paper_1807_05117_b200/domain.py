@@ -4,7 +4,7 @@
 (``blreg/domain.py:19-63``) and adds three B200 options:
 
 * ``pad``  — pad-grid points per axis for truncated convolutions.  The
-  reference uses ``next_fast_len(4K+1)`` (``spectral.py:239-242``); any
+  reference uses ``next_fast_len(4K+1)`` (``spectral.py:142-145``); any
   ``P >= 3K+1`` gives the exact truncated convolution because every pad-grid
   product is bilinear in K-band fields, so the default is the smallest
   engine length >= 3K+1 (e.g. 100 instead of 132 at K=32, 2.3x fewer points).
@@ -159,7 +159,7 @@ class Domain:
 
 
 def symbol_terms(domain: Domain) -> np.ndarray:
-    """alpha-free per-axis metric symbol terms (spectral.py:339-354), concatenated."""
+    """alpha-free per-axis metric symbol terms (spectral.py:242-257), concatenated."""
     out = []
     for f, n in zip(domain.frequencies(), domain.shape):
         if domain.symbol == "discrete":
@@ -171,38 +171,61 @@ def symbol_terms(domain: Domain) -> np.ndarray:
 
 
 class Context:
-    """Owns one ``blr_ctx`` (cuFFT plans, scratch) for a domain on one device."""
+    """Device contexts (``blr_ctx``: cuFFT plans, engine scratch) for a domain.
+
+    Thread / stream safety (reference contract ``objectives/base.py:69-72``:
+    ``hessian_vector`` may be called concurrently on one evaluation): every
+    (host thread, torch stream) pair gets its own ``blr_ctx``, created on first
+    use with its stream fixed, so no scratch buffer and no host-side state is
+    ever shared between two threads or between two streams.  Work issued by one
+    thread on one stream is stream-ordered, so reusing that handle's scratch
+    from call to call is safe.
+    """
 
     def __init__(self, domain: Domain):
         if not torch.cuda.is_available():
             raise _lib.CudaExtensionMissing("no CUDA device: the B200 path has no CPU fallback")
         self.domain = domain
         self.lib = _lib.load()
+        self._handles = {}  # (thread id, stream) -> blr_ctx*
+        self.lock = threading.Lock()
+
+    def _create(self, stream: int):
+        d = self.domain
         h = C.c_void_p()
-        tab, keep = _lib.double_array(symbol_terms(domain))
-        with torch.cuda.device(domain.device):
+        tab, keep = _lib.double_array(symbol_terms(d))
+        with torch.cuda.device(d.device):
             _lib.check(self.lib.blr_ctx_create(
-                C.byref(h), domain.ndim, _lib.int_array(domain.shape),
-                _lib.int_array(domain.bandwidth), _lib.int_array(domain.pad), float(domain.alpha),
-                int(domain.order), tab, 0 if domain.dtype == "float64" else 1, int(domain.device)),
-                "blr_ctx_create")
+                C.byref(h), d.ndim, _lib.int_array(d.shape), _lib.int_array(d.bandwidth),
+                _lib.int_array(d.pad), float(d.alpha), int(d.order), tab,
+                0 if d.dtype == "float64" else 1, int(d.device)), "blr_ctx_create")
+            _lib.check(self.lib.blr_set_stream(h, C.c_void_p(stream)), "blr_set_stream")
         del keep
-        self.h = h
-        self._stream = None
-        self.lock = threading.RLock()
+        return h
 
     def bind(self):
-        """Point the context at the caller's current torch stream; returns the handle."""
+        """The handle for the calling thread on its current torch stream of
+        ``domain.device``.  Entry points make the context's device current
+        themselves (``blr_capi.cu`` DISPATCH), so callers need not."""
         s = torch.cuda.current_stream(self.domain.device).cuda_stream
-        if s != self._stream:
-            _lib.check(self.lib.blr_set_stream(self.h, C.c_void_p(s)), "blr_set_stream")
-            self._stream = s
-        return self.h
+        key = (threading.get_ident(), s)
+        h = self._handles.get(key)
+        if h is None:
+            with self.lock:
+                h = self._handles.get(key)
+                if h is None:
+                    h = self._create(s)
+                    self._handles[key] = h
+        return h
+
+    @property
+    def n_handles(self) -> int:
+        return len(self._handles)
 
     def __del__(self):
         try:
-            if getattr(self, "h", None):
-                self.lib.blr_ctx_destroy(self.h)
+            for h in self._handles.values():
+                self.lib.blr_ctx_destroy(h)
         except Exception:
             pass
 

@@ -96,7 +96,7 @@ def include(domain: Domain, coeffs, grid_shape=None, check: bool = True, deriv=N
     ``deriv`` (optional, one entry per realized field): component axis ``j``
     realizes ``d_j`` of the field (``spectral_gradient`` fused), -1 none.
     Raises ``ValueError`` when the symmetry violation exceeds 1e-10
-    (``spectral.py:103-108``).
+    (``spectral.py:104-105``).
     """
     d = domain.ndim
     c = as_band(domain, coeffs)
@@ -171,7 +171,7 @@ def conv_dot(domain: Domain, a, b) -> torch.Tensor:
 
 
 def truncated_convolution(domain: Domain, a, b) -> torch.Tensor:
-    """Dispatch on operand rank (spectral.py:253-275)."""
+    """Dispatch on operand rank (spectral.py:156-178)."""
     d = domain.ndim
     ra, rb = a.ndim - d, b.ndim - d
     if ra == 0 and rb == 0:
@@ -188,7 +188,7 @@ def truncated_convolution(domain: Domain, a, b) -> torch.Tensor:
 
 
 # ---------------------------------------------------------------------------
-# diagonal operators (spectral.py:321-425)
+# diagonal operators (spectral.py:242-328)
 # ---------------------------------------------------------------------------
 
 def _angular_frequencies(domain: Domain):
@@ -202,7 +202,7 @@ def _angular_frequencies(domain: Domain):
 
 
 def metric_symbol(domain: Domain) -> np.ndarray:
-    """Host copy of ``A(k)**order`` (spectral.py:357-359)."""
+    """Host copy of ``A(k)**order`` (spectral.py:260-262)."""
     acc = np.zeros(domain.block_shape, dtype=np.float64)
     for ax, (f, n) in enumerate(zip(domain.frequencies(), domain.shape)):
         shape = [1] * domain.ndim
@@ -277,7 +277,7 @@ def make_divergence_free(domain: Domain, vec) -> torch.Tensor:
 
 
 # ---------------------------------------------------------------------------
-# inner products and norms (spectral.py:432-447)
+# inner products and norms (spectral.py:335-350)
 # ---------------------------------------------------------------------------
 
 def inner(a, b, domain: Domain | None = None) -> float:

@@ -203,6 +203,109 @@ def checksum_case(name, n, k):
     save(name, **dom_meta(dom), **out)
 
 
+N_SAMPLES = 1000
+
+
+def _vector_summary(prefix, x, w, r, idx):
+    """Full-precision fingerprint of one band vector (a few KB, not 13 MB):
+    Frobenius norm, Re<x, w>, Re<x, r> against a seeded probe, and the complex
+    coefficients at ``idx`` (flat indices into ``x``)."""
+    return {f"{prefix}_norm": np.linalg.norm(x), f"{prefix}_dot_w": spectral.inner(x, w),
+            f"{prefix}_dot_r": spectral.inner(x, r), f"{prefix}_samples": x.reshape(-1)[idx]}
+
+
+def headline_probe(shape):
+    """Seeded probe vector and sample indices shared by the generator and the
+    GPU test (plain numpy, so the GPU box regenerates them bit-identically)."""
+    rng = np.random.default_rng(20260)
+    r = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    idx = np.sort(rng.choice(int(np.prod(shape)), N_SAMPLES, replace=False))
+    return r, idx
+
+
+def headline_case(tag):
+    """BASELINE config 3 at full precision: 128³/K=32,
+    Nt=10, the §8(d) micro-benchmark recipe, one objective per process
+    (~20 CPU-minutes each).  Energy, gradient, GN and Newton HVP."""
+    n, k = 128, 32
+    dom = Domain((n,) * 3, (k,) * 3, alpha=0.02, order=2)
+    rng = np.random.default_rng(0)
+    I0, I1 = band_image(dom, rng), band_image(dom, rng)
+    v = TimeFlow(dom, smooth_vector_block(dom, rng, 0.5 / n, decay=2.0)[None], 10, True)
+    w = TimeFlow(dom, smooth_vector_block(dom, rng, 0.5 / n, decay=2.0)[None], 10, True)
+    cfg = ProblemConfig(sigma2=0.1, n_time_steps=10)
+    cls = {"state": StateObjective, "def": DeformationObjective}[tag]
+    r, idx = headline_probe(v.values.shape)
+    obj = cls(dom, I0, I1, cfg)
+    out = dict(n=n, k=k, sample_idx=idx)
+    t0 = time.perf_counter()
+    out["energy_direct"] = obj.energy(v)
+    ev = obj.gradient(v)
+    out["energy"], out["reg_energy"], out["data_energy"] = ev.energy, ev.reg_energy, ev.data_energy
+    out["substeps"] = ev.cache.substeps
+    out.update(_vector_summary("grad", ev.gradient.values, w.values, r, idx))
+    out["t_grad_s"] = time.perf_counter() - t0
+    for gn, name in ((True, "hvp_gn"), (False, "hvp_newton")):
+        t0 = time.perf_counter()
+        hw = ev.hessian_vector(w, gauss_newton=gn).values
+        out[f"t_{name}_s"] = time.perf_counter() - t0
+        out.update(_vector_summary(name, hw, w.values, r, idx))
+        print(f"  headline_128/{tag}/{name}: {out[f't_{name}_s']:.0f}s", flush=True)
+    save(f"headline_128_{tag}", **dom_meta(dom), **out)
+
+
+def blob_pair_ref(dom, seed=1):
+    """Seeded 3-D pair (the bench's ``blob_pair`` recipe) built with the
+    reference's own helpers: six periodic bumps; target = cubic warp of the
+    source by a band-4 smooth displacement of ~3 voxels."""
+    n = dom.shape[0]
+    rng = np.random.default_rng(seed)
+    axes = [np.arange(s) / s for s in dom.shape]
+    mesh = np.meshgrid(*axes, indexing="ij")
+    src = np.zeros(dom.shape)
+    for _ in range(6):
+        c = 0.3 + 0.4 * rng.random(3)
+        sharp = 8.0 + 16.0 * rng.random()
+        b = np.ones(dom.shape)
+        for x, cc in zip(mesh, c):
+            b = b * np.exp(sharp * (np.cos(2 * np.pi * (x - cc)) - 1.0))
+        src += (0.5 + 0.5 * rng.random()) * b
+    src /= src.max()
+    ddom = Domain(dom.shape, (4,) * dom.ndim)
+    disp = spectral.include(ddom, smooth_vector_block(ddom, rng, 3.0 / n, decay=2.0))
+    return src, gridops.warp(ddom, src, disp, interp="cubic")
+
+
+def config2_case(tag):
+    """SURVEY config 2 end to end: 3-D 64³/K=16 blob pair,
+    alpha=0.01, s=2, sigma²=0.03, ``SolverConfig()`` defaults, one objective
+    per process."""
+    dom = Domain((64,) * 3, (16,) * 3, alpha=0.01, order=2)
+    source, target = blob_pair_ref(dom)
+    cls = {"state": StateObjective, "def": DeformationObjective}[tag]
+    obj = cls(dom, source, target, ProblemConfig(sigma2=0.03))
+    t0 = time.perf_counter()
+    res = minimize(obj, TimeFlow.zero(dom), SolverConfig())
+    wall = time.perf_counter() - t0
+    jd = gridops.jacobian_determinant(
+        dom, spectral.include(dom, res.evaluation.cache.forward[-1], check=False))
+    r, idx = headline_probe(res.velocity.values.shape)
+    out = dict(source=source, target=target, status=res.status,
+               energy=np.array([x.energy for x in res.records]),
+               pcg=np.array([x.pcg_iters for x in res.records]),
+               step=np.array([x.step for x in res.records]),
+               negc=np.array([x.negative_curvature for x in res.records]),
+               mse=np.array([x.mse_rel for x in res.records]),
+               grel=np.array([x.grad_rel for x in res.records]),
+               final_mse=res.final_mse_rel, final_grad_rel=res.final_grad_rel,
+               final_energy=res.evaluation.energy, total_pcg=res.total_pcg_iters,
+               jmin=float(jd.min()), jmax=float(jd.max()), wall_s=wall,
+               sample_idx=idx, velocity_norm=np.linalg.norm(res.velocity.values),
+               velocity_samples=res.velocity.values.reshape(-1)[idx])
+    print(f"  config2_64/{tag}: {res.status} {len(res.records)} records, {wall:.0f}s", flush=True)
+    save(f"config2_64_{tag}", **dom_meta(dom), **out)
+
+
 def volio_case(name):
     """BLVOL files written by the reference writer (volio.py), stored as bytes."""
     import tempfile
@@ -223,6 +326,12 @@ def volio_case(name):
 
 
 def main():
+    if "--headline" in sys.argv:  # --headline state|def (one objective per process)
+        headline_case(sys.argv[sys.argv.index("--headline") + 1])
+        return
+    if "--config2" in sys.argv:  # --config2 state|def
+        config2_case(sys.argv[sys.argv.index("--config2") + 1])
+        return
     slow = "--slow" in sys.argv
     spectral_case("spectral_3d", Domain((12, 16, 18), (3, 4, 5), alpha=0.05), 1)
     spectral_case("spectral_2d", Domain((32, 30), (8, 7), alpha=0.05), 2)

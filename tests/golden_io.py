@@ -29,3 +29,16 @@ def rel(a, b):
     den = np.linalg.norm(b.ravel())
     num = np.linalg.norm((a - b).ravel())
     return num / den if den > 0 else num
+
+
+N_SAMPLES = 1000
+
+
+def headline_probe(shape):
+    """Seeded probe vector and coefficient-sample indices of the full-precision
+    fixtures (must match ``make_golden.headline_probe``; checked on the CPU by
+    ``test_oracle_golden.test_headline_probe_matches_fixture``)."""
+    rng = np.random.default_rng(20260)
+    r = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    idx = np.sort(rng.choice(int(np.prod(shape)), N_SAMPLES, replace=False))
+    return r, idx

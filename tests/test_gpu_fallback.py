@@ -75,9 +75,10 @@ def test_objective_on_cufft_path(name, kind, padf):
     assert rel(np_(ev.hessian_vector(w, gauss_newton=False).values), g[f"{kind}_hvp_newton"]) < 1e-10
 
 
-@pytest.mark.parametrize("N,K,alt", [(136, 64, 198), (48, 20, 66), (40, 16, 54)])
+@pytest.mark.parametrize("N,K,alt", [(136, 64, 198), (128, 32, 98), (48, 20, 66), (40, 16, 54)])
 def test_engine_lengths_match_cufft(N, K, alt):
-    """The largest engine lengths (196 = 14x14, 64, 50) against the cuFFT path
+    """The largest engine lengths (196 = 14x14, 100 = the benchmarked
+    128^3/K=32 instantiation, 64, 50) against the cuFFT path
     at another exact pad: both are the exact truncated convolution, so energy,
     gradient and GN / Newton HVPs agree to round-off (3-D, deformation)."""
     import bench

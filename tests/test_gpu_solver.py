@@ -51,6 +51,38 @@ def test_config1_registration_trace(kind):
                                rtol=e_tol * 10)
 
 
+@pytest.mark.parametrize("kind", ["def", "state"])
+def test_config2_registration_trace(kind):
+    """SURVEY config 2 end to end (3-D 64^3, K=16, alpha 0.01, sigma2 0.03,
+    SolverConfig() defaults) on the seeded blob pair the reference registered
+    (make_golden --config2): identical discrete trace, final values within the
+    SURVEY §8(d) end-to-end tolerances."""
+    name = f"config2_64_{kind}"
+    if not exists(name):
+        pytest.skip("fixture needs make_golden --config2")
+    g = load(name)
+    dom = B.Domain((64,) * 3, (16,) * 3, alpha=0.01, order=2)
+    cls = B.DeformationObjective if kind == "def" else B.StateObjective
+    obj = cls(dom, g["source"], g["target"], B.ProblemConfig(sigma2=0.03))
+    res = B.minimize(obj, B.TimeFlow.zero(dom), B.SolverConfig())
+    assert res.status == str(g["status"])
+    assert [r.pcg_iters for r in res.records] == list(g["pcg"])
+    assert [r.negative_curvature for r in res.records] == list(g["negc"])
+    assert [r.step for r in res.records] == list(g["step"])
+    assert res.total_pcg_iters == int(g["total_pcg"])
+    e_tol, m_tol, j_tol = (1e-9, 1e-8, 1e-8) if kind == "def" else (1e-4, 1e-4, 1e-3)
+    assert res.evaluation.energy == pytest.approx(float(g["final_energy"]), rel=e_tol)
+    assert res.final_mse_rel == pytest.approx(float(g["final_mse"]), rel=m_tol)
+    np.testing.assert_allclose([r.energy for r in res.records], g["energy"], rtol=e_tol * 10)
+    jd = gridops.jacobian_determinant(dom, spectral.include(dom, res.evaluation.cache.forward[-1],
+                                                             check=False))
+    assert float(jd.min()) == pytest.approx(float(g["jmin"]), rel=j_tol)
+    assert float(jd.max()) == pytest.approx(float(g["jmax"]), rel=j_tol)
+    vel = res.velocity.values.cpu().numpy().reshape(-1)[g["sample_idx"]]
+    ref = g["velocity_samples"]
+    assert np.linalg.norm(vel - ref) <= (e_tol * 10) ** 0.5 * np.linalg.norm(ref)
+
+
 @pytest.mark.skipif(not exists("checksum_64"), reason="fixture needs make_golden --slow")
 @pytest.mark.parametrize("kind", ["state", "def"])
 def test_checksum_64(kind):

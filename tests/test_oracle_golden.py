@@ -132,3 +132,18 @@ def test_checksum_64(kind):
     assert ev.energy == pytest.approx(float(g[f"{kind}_energy"]), rel=1e-12)
     hw = obj.hessian_vector(ev, w, True).values
     assert np.linalg.norm(hw) == pytest.approx(float(g[f"{kind}_hvp_norm"]), rel=1e-10)
+
+
+@pytest.mark.parametrize("name", ["headline_128_state", "headline_128_def", "config2_64_state",
+                                  "config2_64_def"])
+def test_headline_probe_matches_fixture(name):
+    """The GPU tests regenerate the seeded probe / sample indices; they must be
+    the ones the reference-side generator used."""
+    if not exists(name):
+        pytest.skip("fixture needs make_golden --headline / --config2")
+    from golden_io import headline_probe
+
+    g = load(name)
+    shape = (1, 3, 65, 65, 65) if name.startswith("headline") else (1, 3, 33, 33, 33)
+    _, idx = headline_probe(shape)
+    assert np.array_equal(idx, g["sample_idx"])
