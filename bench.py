@@ -327,14 +327,19 @@ def survey_model_bytes(args, dom):
     return float(F * 2 * S * (P3 + B3) + X * 2 * S * (N3 + B3) + G * S * N3)
 
 
-def ncu_traffic():
-    """Per-category DRAM bytes per launch from the committed ncu capture, if any."""
+def ncu_traffic(workload_name, dtype, pad, kernel):
+    """DRAM bytes per launch of ``kernel`` from a committed ncu capture of
+    exactly this workload / dtype / pad (profiles/ncu_traffic.json), else None."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f)
+            caps = json.load(f)["captures"]
     except Exception:
-        return {}
+        return None
+    for c in caps:
+        if (c["workload"], c["dtype"], list(c["pad"]), c["kernel"]) == (workload_name, dtype, list(pad), kernel):
+            return c["traffic"]
+    return None
 
 
 def run_b200(args, rank, world, local):
@@ -465,7 +470,6 @@ def run_b200(args, rank, world, local):
 
     # roofline of the dominant kernel category (live CUDA events)
     peak, peak_kind = peaks()
-    traffic = ncu_traffic()
     total_prof_ms = sum(v[1] for v in prof.values())
     breakdown = {k: {"launches": int(v[0]), "ms": round(v[1], 4),
                      "share": round(v[1] / total_prof_ms, 4) if total_prof_ms else None,
@@ -474,7 +478,8 @@ def run_b200(args, rank, world, local):
     dom_name, dv = max(prof.items(), key=lambda kv: kv[1][1])
     n_launch, ms, nbytes = dv
     achieved = nbytes / n_launch / (ms / n_launch * 1e-3) / 1e9
-    tr = traffic.get(dom_name)
+    tr = ncu_traffic(workload(args)["workload"], "f64" if args.dtype == "float64" else "f32", list(dom.pad),
+                     dom_name)
     roofline = {"bound": "hbm", "kernel": dom_name, "achieved": round(achieved, 1), "peak": peak,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
                 "traffic": tr, "algorithmic_bytes_per_launch": nbytes / n_launch,

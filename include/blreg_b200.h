@@ -175,6 +175,19 @@ int blr_mul(blr_ctx* ctx, const void* a, const void* b, int64_t n, void* out);
  * weights NULL -> per-node outputs [n_nodes][d][N^3] */
 int blr_state_data(blr_ctx* ctx, const void* vol, const void* lamw, const void* gm,
                    int n_nodes, const double* weights, void* out);
+/* full-Newton state data term (state.py:138-154), one pass over the nodes:
+ *   dm_k = sgw_k . dphi_k,  dl_k = dlam o (id + psi_k)  (or the given dl [n][N^3]),
+ *   dlam_k = dvol_k aew_k + vol_k (agw_k . dpsi_k) + vol_k dl_k,
+ *   term_k = dlam_k wg_k + vol_k aew_k grad(dm_k)   (grad_mode 0 central, 1 spectral)
+ * out = sum_k w_k term_k [d][N^3], or weights NULL -> per node [n][d][N^3].
+ * scalars [n][N^3]: vol, aew, dvol; vectors [n][d][N^3]: agw, dpsi, psi, wg, sgw, dphi */
+int blr_state_newton(blr_ctx* ctx, const void* dlam, const void* dl, int interp, const void* vol,
+                     const void* aew, const void* dvol, const void* agw, const void* dpsi,
+                     const void* psi, const void* wg, const void* sgw, const void* dphi, int n_nodes,
+                     const double* weights, int grad_mode, void* out);
+/* out[a] += s * sum_b H[a][b] u[b]  (deformation.py:141-145, transposed Newton endpoint
+ * term, H [d][d][N^3]); H NULL -> out[a] += s * u[a] */
+int blr_lam_matvec_add(blr_ctx* ctx, const void* s, const void* H, const void* u, void* out);
 
 #ifdef __cplusplus
 }

@@ -60,6 +60,8 @@ SIGNATURES = {
     "blr_scaled_diff": [_vp, _vp, _vp, _d, _vp],
     "blr_mul": [_vp, _vp, _vp, _i64, _vp],
     "blr_state_data": [_vp, _vp, _vp, _vp, _i, _dp, _vp],
+    "blr_state_newton": [_vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _dp, _i, _vp],
+    "blr_lam_matvec_add": [_vp, _vp, _vp, _vp, _vp],
 }
 _RESTYPES = {"blr_last_error": C.c_char_p, "blr_launch_count": C.c_int64}
 

@@ -434,4 +434,25 @@ int blr_state_data(blr_ctx* c, const void* vol, const void* lamw, const void* gm
   });
 }
 
+
+int blr_state_newton(blr_ctx* c, const void* dlam, const void* dl, int interp, const void* vol,
+                     const void* aew, const void* dvol, const void* agw, const void* dpsi, const void* psi,
+                     const void* wg, const void* sgw, const void* dphi, int n_nodes, const double* weights,
+                     int grad_mode, void* out) {
+  return guarded([&] {
+    need(c && vol && aew && dvol && agw && dpsi && wg && sgw && dphi && out && n_nodes >= 1, "bad arguments");
+    need(dl || (dlam && psi && interp >= 0 && interp <= 3), "need dl, or dlam + psi with a grid interp");
+    need(grad_mode == 0 || grad_mode == 1, "grad_mode must be 0 (central) or 1 (spectral)");
+    DISPATCH(c, state_newton<T>(c, (const T*)dlam, (const T*)dl, interp, (const T*)vol, (const T*)aew,
+                                (const T*)dvol, (const T*)agw, (const T*)dpsi, (const T*)psi, (const T*)wg,
+                                (const T*)sgw, (const T*)dphi, n_nodes, weights, grad_mode, (T*)out));
+  });
+}
+
+int blr_lam_matvec_add(blr_ctx* c, const void* s, const void* H, const void* u, void* out) {
+  return guarded([&] {
+    need(c && s && u && out, "bad arguments");
+    DISPATCH(c, lam_matvec_add<T>(c, (const T*)s, (const T*)H, (const T*)u, (T*)out));
+  });
+}
 }  // extern "C"

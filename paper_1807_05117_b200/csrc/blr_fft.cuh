@@ -396,16 +396,92 @@ struct WShape {
   static constexpr int L = R1 * R2;
   static constexpr int RM = R1 > R2 ? R1 : R2;
   static constexpr int LPW = 32 / RM;               // lines per warp
-  static constexpr int TS = R1 * (R2 + 1);          // shared tile entries per line
-  static constexpr int TILE = LPW * TS;             // shared tile entries per warp
 };
 
+// --- shared-memory bank model ----------------------------------------------
+// A warp request of E-byte accesses is served in phases of 128/E lanes; a
+// phase costs the largest number of distinct 4-byte words any one bank must
+// deliver (same word = broadcast).  ncu's "L1 Wavefronts Shared" match this
+// model on the r02 captures (tile stores 1.50x ideal, twiddle loads 2.5x).
+// addr(lane) < 0: inactive lane.
+template <class F>
+constexpr int wavefronts(F addr, int E) {
+  const int per = 128 / E, words = E / 4;
+  int tot = 0;
+  for (int p0 = 0; p0 < 32; p0 += per) {
+    int uniq[32] = {}, nu = 0;  // distinct element addresses of the phase
+    for (int lane = p0; lane < p0 + per; ++lane) {
+      const int a = addr(lane);
+      bool dup = a < 0;
+      for (int q = 0; q < nu && !dup; ++q) dup = uniq[q] == a;
+      if (!dup) uniq[nu++] = a;
+    }
+    int cnt[32] = {};
+    for (int q = 0; q < nu; ++q)
+      for (int w = 0; w < words; ++w) ++cnt[(uniq[q] * words + w) % 32];
+    int worst = 0;
+    for (int b = 0; b < 32; ++b) worst = cnt[b] > worst ? cnt[b] : worst;
+    tot += worst;
+  }
+  return tot;
+}
+
+// Per-warp FFT tile [line][k1][n2] at line * TS + k1 * KS + n2, strides chosen
+// by the bank model for the step-A stores and step-B loads (fp64: 80
+// wavefronts per L=100 transform instead of 100 with the dense R2+1 stride).
+template <class S>
+constexpr int tile_cost(int TS, int KS, int E) {
+  int c = 0;
+  for (int k1 = 0; k1 < S::R1; ++k1)
+    c += wavefronts([&](int l) { return l / S::R2 < S::LPW ? (l / S::R2) * TS + k1 * KS + l % S::R2 : -1; }, E);
+  for (int n2 = 0; n2 < S::R2; ++n2)
+    c += wavefronts([&](int l) { return l / S::R1 < S::LPW ? (l / S::R1) * TS + (l % S::R1) * KS + n2 : -1; }, E);
+  return c;
+}
+// BLR_BANKPAD=1 selects the bank-model strides; the default keeps the dense
+// tile (KS = R2 + 1).  A/B on the B200 (r02): the conflict-free layout cut the
+// z-line kernels' shared wavefronts by 30-45% but not their time (they are
+// latency-bound at 8-12 warps per SM), and its larger footprint cost the
+// outer op a CTA per SM, so it is off.
+#ifndef BLR_BANKPAD
+#define BLR_BANKPAD 0
+#endif
+template <typename T, class S>
+struct TileG {
+  static constexpr int E = (int)(2 * sizeof(T));
+  static constexpr int best() {  // KS * 256 + TS
+    if (!BLR_BANKPAD) return (S::R2 + 1) * 256 + S::R1 * (S::R2 + 1);
+    int bc = 1 << 30, bv = 0;
+    for (int ks = S::R2; ks < S::R2 + 8; ++ks) {
+      const int base = (S::R1 - 1) * ks + S::R2;
+      for (int ts = base; ts < base + 8; ++ts) {
+        const int c = tile_cost<S>(ts, ks, E);
+        if (c < bc) { bc = c; bv = ks * 256 + ts; }
+      }
+    }
+    return bv;
+  }
+  static constexpr int KS = best() / 256;
+  static constexpr int TS = best() % 256;          // shared tile entries per line
+  static constexpr int TILE = S::LPW * TS;         // shared tile entries per warp
+};
+
+// Step-A twiddles W_L^(k1 n2) are read from a split table of T: real parts at
+// twr[k1 * R2 + n2], imaginary parts at twr[L + k1 * R2 + n2].  Lanes of a
+// request differ in n2 only, so the two 8-byte (fp64) loads are conflict-free
+// (the packed table tw[k1 * n2] cost 2.4x the ideal wavefronts).
+template <typename T, class S>
+__device__ __forceinline__ Cx<T> twiddle(const T* twr, int k1, int n2) {
+  return cx<T>(twr[k1 * S::R2 + n2], twr[S::L + k1 * S::R2 + n2]);
+}
+
 // step A: lanes (line, n2) gather x[R2*n1 + n2] with load(line, n, n1), DFT_R1,
-// twiddle W_L^(n2 k1) (table tw[m] = exp(-2 pi i m / L)), store to the tile.
+// twiddle W_L^(n2 k1), store to the tile.
 // ALIAS: the tile overlays the warp's own input lines in shared memory, so all
 // lanes finish loading before any lane stores.
 template <typename T, class S, bool INV, bool ALIAS = false, class Load>
-__device__ __forceinline__ void wfft_a(Cx<T>* tile, const Cx<T>* tw, int nl, Load& load) {
+__device__ __forceinline__ void wfft_a(Cx<T>* tile, const T* twr, int nl, Load& load) {
+  using G = TileG<T, S>;
   const int lane = threadIdx.x & 31;
   const int line = lane / S::R2, n2 = lane - (lane / S::R2) * S::R2;
   const bool act = line < nl && line < S::LPW;
@@ -417,16 +493,16 @@ __device__ __forceinline__ void wfft_a(Cx<T>* tile, const Cx<T>* tw, int nl, Loa
   if (ALIAS) __syncwarp();
   if (act) {
     dft<T, S::R1, INV>(v);
-    Cx<T>* t = tile + line * S::TS + n2;
+    Cx<T>* t = tile + line * G::TS + n2;
 #pragma unroll
     for (int k1 = 0; k1 < S::R1; ++k1) {
       Cx<T> z = v[k1];
       if (k1 * n2 != 0) {
-        Cx<T> w = tw[k1 * n2];
+        Cx<T> w = twiddle<T, S>(twr, k1, n2);
         if (INV) w.y = -w.y;
         z = cmul(z, w);
       }
-      t[k1 * (S::R2 + 1)] = z;
+      t[k1 * G::KS] = z;
     }
   }
   __syncwarp();
@@ -436,11 +512,12 @@ __device__ __forceinline__ void wfft_a(Cx<T>* tile, const Cx<T>* tw, int nl, Loa
 // store(line, k, value) (k2 ascending).
 template <typename T, class S, bool INV, class Store>
 __device__ __forceinline__ void wfft_b(const Cx<T>* tile, int nl, Store& store) {
+  using G = TileG<T, S>;
   const int lane = threadIdx.x & 31;
   const int line = lane / S::R1, k1 = lane - (lane / S::R1) * S::R1;
   if (line < nl && line < S::LPW) {
     Cx<T> u[S::R2];
-    const Cx<T>* t = tile + line * S::TS + k1 * (S::R2 + 1);
+    const Cx<T>* t = tile + line * G::TS + k1 * G::KS;
 #pragma unroll
     for (int n2 = 0; n2 < S::R2; ++n2) u[n2] = t[n2];
     dft<T, S::R2, INV>(u);
@@ -451,8 +528,8 @@ __device__ __forceinline__ void wfft_b(const Cx<T>* tile, int nl, Store& store) 
 }
 
 template <typename T, class S, bool INV, bool ALIAS = false, class Load, class Store>
-__device__ __forceinline__ void wfft(Cx<T>* tile, const Cx<T>* tw, int nl, Load load, Store store) {
-  wfft_a<T, S, INV, ALIAS>(tile, tw, nl, load);
+__device__ __forceinline__ void wfft(Cx<T>* tile, const T* twr, int nl, Load load, Store store) {
+  wfft_a<T, S, INV, ALIAS>(tile, twr, nl, load);
   wfft_b<T, S, INV>(tile, nl, store);
 }
 
@@ -488,6 +565,13 @@ __device__ __forceinline__ void wfft(Cx<T>* tile, const Cx<T>* tw, int nl, Load 
   X(64, 8, 8)              \
   X(100, 10, 10)           \
   X(196, 14, 14)
+
+inline int shape_r2(int L) {
+#define BLR_CASE(LL, A, B) if (L == LL) return B;
+  BLR_FOR_EACH_L(BLR_CASE)
+#undef BLR_CASE
+  return 1;
+}
 
 inline bool supported_len(int L) {
 #define BLR_CASE(LL, A, B) if (L == LL) return true;

@@ -490,6 +490,158 @@ void state_data(blr_ctx* c, const T* vol, const T* lamw, const T* gm, int n_node
   if (dw) BLR_CUDA(cudaFreeAsync(dw, c->stream));
 }
 
+
+// ---------------------------------------------------------------------------
+// full-Newton data terms (no torch-eager node loops)
+// ---------------------------------------------------------------------------
+// dm[k] = sum_a g[k][a] u[k][a] for n_nodes nodes (state.py:143: dm = sgw . dphi)
+template <typename T>
+__global__ void k_dot_nodes(const T* __restrict__ g, const T* __restrict__ u, int n_nodes, FullDesc fd,
+                            T* __restrict__ out) {
+  const int64_t total = fd.nn * n_nodes;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(idx / fd.nn);
+    const int64_t i = idx - k * fd.nn, od = (int64_t)k * fd.d * fd.nn + i;
+    T s = 0;
+    for (int a = 0; a < fd.d; ++a) s += g[od + a * fd.nn] * u[od + a * fd.nn];
+    out[idx] = s;
+  }
+}
+
+// Full-Newton state data term at node k (state.py:138-154):
+//   dlam_k = dvol_k aew_k + vol_k (agw_k . dpsi_k) + vol_k dl_k,   dl_k = dlam1 o (id + psi_k)
+//   term_k = dlam_k wg_k + (vol_k aew_k) grad(dm_k)
+// summed with weights w_k (stationary; one projection afterwards) or written per node.
+// grad(dm_k): central differences of dm (gridops.py:84-89) or the precomputed gdm.
+template <typename T>
+__global__ void __launch_bounds__(256) k_state_newton(
+    const T* __restrict__ dlam, const T* __restrict__ dl, int interp, const T* __restrict__ vol,
+    const T* __restrict__ aew, const T* __restrict__ dvol, const T* __restrict__ agw,
+    const T* __restrict__ dpsi, const T* __restrict__ psi, const T* __restrict__ wg,
+    const T* __restrict__ dm, const T* __restrict__ gdm, int n_nodes, NodeW w, int use_w, FullDesc fd,
+    int add, T* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < fd.nn;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int x[3];
+    unravel(fd, i, x);
+    T s[3] = {0, 0, 0};
+    for (int k = 0; k < n_nodes; ++k) {
+      const int64_t o1 = (int64_t)k * fd.nn + i, od = (int64_t)k * fd.d * fd.nn + i;
+      T dlk;
+      if (dl) {
+        dlk = dl[o1];
+      } else {
+        double c[3];
+        sample_coords<T>(fd, psi + (int64_t)k * fd.d * fd.nn, i, x, c);
+        dlk = (T)interp_at<T>(dlam, fd, c, interp);
+      }
+      const T vk = vol[o1], ak = aew[o1];
+      T ad = 0;
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        if (b < fd.d) ad += agw[od + b * fd.nn] * dpsi[od + b * fd.nn];
+      const T q = dvol[o1] * ak + vk * ad + vk * dlk;
+      const T lam = vk * ak;
+      const T* dmk = dm + (int64_t)k * fd.nn;
+#pragma unroll
+      for (int comp = 0; comp < 3; ++comp) {
+        if (comp >= fd.d) continue;
+        T G;
+        if (gdm) {
+          G = gdm[od + comp * fd.nn];
+        } else {
+          const int ax = 3 - fd.d + comp;
+          int xp[3] = {x[0], x[1], x[2]}, xm[3] = {x[0], x[1], x[2]};
+          xp[ax] = x[ax] + 1 == fd.N[ax] ? 0 : x[ax] + 1;
+          xm[ax] = x[ax] == 0 ? fd.N[ax] - 1 : x[ax] - 1;
+          const T denom = (T)(2.0 * (1.0 / fd.N[ax]));
+          G = (dmk[ravel(fd, xp[0], xp[1], xp[2])] - dmk[ravel(fd, xm[0], xm[1], xm[2])]) / denom;
+        }
+        const T term = q * wg[od + comp * fd.nn] + lam * G;
+        if (use_w) s[comp] += (T)w.w[k] * term;
+        else out[od + comp * fd.nn] = term;
+      }
+    }
+    if (use_w) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        if (a < fd.d) out[a * fd.nn + i] = add ? out[a * fd.nn + i] + s[a] : s[a];
+    }
+  }
+}
+
+template <typename T>
+void state_newton(blr_ctx* c, const T* dlam, const T* dl, int interp, const T* vol, const T* aew, const T* dvol,
+                  const T* agw, const T* dpsi, const T* psi, const T* wg, const T* sgw, const T* dphi,
+                  int n_nodes, const double* weights, int grad_mode, T* out) {
+  FullDesc fd = full_desc(c->g);
+  T *dm = nullptr, *gdm = nullptr, *coef = nullptr;
+  BLR_CUDA(cudaMallocAsync((void**)&dm, (size_t)n_nodes * fd.nn * sizeof(T), c->stream));
+  k_dot_nodes<T><<<grid_blocks(fd.nn * n_nodes, 256), 256, 0, c->stream>>>(sgw, dphi, n_nodes, fd, dm);
+  BLR_LAUNCHED();
+  if (grad_mode != 0) {
+    BLR_CUDA(cudaMallocAsync((void**)&gdm, (size_t)n_nodes * fd.d * fd.nn * sizeof(T), c->stream));
+    grid_gradient<T>(c, dm, n_nodes, grad_mode, gdm);
+  }
+  const T* src = dlam;
+  if (!dl && interp == 3) {
+    BLR_CUDA(cudaMallocAsync((void**)&coef, fd.nn * sizeof(T), c->stream));
+    bspline_prefilter<T>(c, dlam, 1, coef);
+    src = coef;
+  }
+  ProfScope ps(c, "state_newton", (double)fd.nn * n_nodes * (6 + 5 * fd.d) * sizeof(T));
+  const int64_t nd = (int64_t)fd.d * fd.nn;
+  if (!weights) {
+    NodeW dw{};
+    k_state_newton<T><<<grid_blocks(fd.nn, 256), 256, 0, c->stream>>>(
+        src, dl, interp, vol, aew, dvol, agw, dpsi, psi, wg, dm, gdm, n_nodes, dw, 0, fd, 0, out);
+    BLR_LAUNCHED();
+  } else {
+    for (int k0 = 0; k0 < n_nodes; k0 += kMaxNodeW) {  // node chunks: weights ride in the parameters
+      const int nk = std::min(kMaxNodeW, n_nodes - k0);
+      NodeW dw;
+      for (int k = 0; k < nk; ++k) dw.w[k] = weights[k0 + k];
+      k_state_newton<T><<<grid_blocks(fd.nn, 256), 256, 0, c->stream>>>(
+          src, dl ? dl + k0 * fd.nn : nullptr, interp, vol + k0 * fd.nn, aew + k0 * fd.nn, dvol + k0 * fd.nn,
+          agw + k0 * nd, dpsi + k0 * nd, psi + k0 * nd, wg + k0 * nd, dm + k0 * fd.nn,
+          gdm ? gdm + k0 * nd : nullptr, nk, dw, 1, fd, k0 > 0 ? 1 : 0, out);
+      BLR_LAUNCHED();
+    }
+  }
+  BLR_CUDA(cudaFreeAsync(dm, c->stream));
+  if (gdm) BLR_CUDA(cudaFreeAsync(gdm, c->stream));
+  if (coef) BLR_CUDA(cudaFreeAsync(coef, c->stream));
+}
+
+// out[a] += s * sum_b H[a][b] u[b]   (deformation.py:141-145, transposed Newton endpoint term)
+// or, H == nullptr, out[a] += s * u[a]   (direct: lam * grad(dm1))
+template <typename T>
+__global__ void k_lam_matvec_add(const T* __restrict__ s, const T* __restrict__ H, const T* __restrict__ u,
+                                 FullDesc fd, T* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < fd.nn;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const T sv = s[i];
+    for (int a = 0; a < fd.d; ++a) {
+      T m;
+      if (H) {
+        m = 0;
+        for (int b = 0; b < fd.d; ++b) m += H[(a * fd.d + b) * fd.nn + i] * u[b * fd.nn + i];
+      } else {
+        m = u[a * fd.nn + i];
+      }
+      out[a * fd.nn + i] += sv * m;
+    }
+  }
+}
+
+template <typename T>
+void lam_matvec_add(blr_ctx* c, const T* s, const T* H, const T* u, T* out) {
+  FullDesc fd = full_desc(c->g);
+  k_lam_matvec_add<T><<<grid_blocks(fd.nn, 256), 256, 0, c->stream>>>(s, H, u, fd, out);
+  BLR_LAUNCHED();
+}
+
 #define BLR_GINST(T)                                                                             \
   template void warp<T>(blr_ctx*, const T*, int, const T*, int, int, T*);                        \
   template void grid_gradient<T>(blr_ctx*, const T*, int, int, T*);                              \
@@ -500,7 +652,11 @@ void state_data(blr_ctx* c, const T* vol, const T* lamw, const T* gm, int n_node
   template void scale_fields<T>(blr_ctx*, const T*, const T*, T*);                               \
   template void scaled_diff<T>(blr_ctx*, const T*, const T*, double, T*);                        \
   template void mul<T>(blr_ctx*, const T*, const T*, int64_t, T*);                               \
-  template void state_data<T>(blr_ctx*, const T*, const T*, const T*, int, const double*, T*);
+  template void state_data<T>(blr_ctx*, const T*, const T*, const T*, int, const double*, T*);   \
+  template void state_newton<T>(blr_ctx*, const T*, const T*, int, const T*, const T*, const T*,  \
+                                const T*, const T*, const T*, const T*, const T*, const T*, int,  \
+                                const double*, int, T*);                                          \
+  template void lam_matvec_add<T>(blr_ctx*, const T*, const T*, const T*, T*);
 BLR_GINST(double)
 BLR_GINST(float)
 

@@ -115,5 +115,10 @@ template <typename T> void scaled_diff(blr_ctx* c, const T* a, const T* b, doubl
 template <typename T> void mul(blr_ctx* c, const T* a, const T* b, int64_t n, T* out);
 template <typename T> void state_data(blr_ctx* c, const T* vol, const T* lamw, const T* gm, int n_nodes,
                                       const double* weights, T* out);
+template <typename T> void state_newton(blr_ctx* c, const T* dlam, const T* dl, int interp, const T* vol,
+                                        const T* aew, const T* dvol, const T* agw, const T* dpsi, const T* psi,
+                                        const T* wg, const T* sgw, const T* dphi, int n_nodes,
+                                        const double* weights, int grad_mode, T* out);
+template <typename T> void lam_matvec_add(blr_ctx* c, const T* s, const T* H, const T* u, T* out);
 
 }  // namespace blr

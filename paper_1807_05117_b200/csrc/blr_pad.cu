@@ -22,6 +22,15 @@ namespace blr {
   extern template void launch_xfwd<float, WShape<A, B>>(blr_ctx*, PadEngine*, const FwdArgs<float>&);
 BLR_FOR_EACH_L(BLR_EXTERN_L)
 #undef BLR_EXTERN_L
+#define BLR_EXTERN_F2(LL, A, B)                                                                        \
+  extern template void launch_fwd2<double, WShape<A, B>>(blr_ctx*, PadEngine*, const Fwd2Args<double>&, int, \
+                                                         int);                                         \
+  extern template void launch_fwd2<float, WShape<A, B>>(blr_ctx*, PadEngine*, const Fwd2Args<float>&, int,   \
+                                                        int);                                          \
+  extern template bool fwd2_fits<double, WShape<A, B>>(const PadGeom&);                                \
+  extern template bool fwd2_fits<float, WShape<A, B>>(const PadGeom&);
+BLR_FOR_EACH_LZ(BLR_EXTERN_F2)
+#undef BLR_EXTERN_F2
 #define BLR_EXTERN_LZ(LL, A, B, OP)                                                                     \
   extern template void launch_lines<double, WShape<A, B>, OP>(blr_ctx*, PadEngine*, const LineArgs<double>&); \
   extern template void launch_lines<float, WShape<A, B>, OP>(blr_ctx*, PadEngine*, const LineArgs<float>&);
@@ -85,16 +94,20 @@ static PadEngine* engine(blr_ctx* c) {
   int dev;
   BLR_CUDA(cudaGetDevice(&dev));
   BLR_CUDA(cudaDeviceGetAttribute(&e.line_smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  // split twiddle tables per axis (blr_fft.cuh twiddle()): W_L^(k1 n2) for
+  // k1 < R1, n2 < R2, real parts then imaginary parts
   for (int a = 0; a < 3; ++a) {
-    const int L = g.P[a];
-    std::vector<double2> tw(L);
-    for (int m = 0; m < L; ++m) {
-      double s, co;
-      sincospi(-2.0 * m / L, &s, &co);
-      tw[m] = make_double2(co, s);
-    }
-    BLR_CUDA(cudaMalloc(&e.tw[a], L * sizeof(double2)));
-    BLR_CUDA(cudaMemcpy(e.tw[a], tw.data(), L * sizeof(double2), cudaMemcpyHostToDevice));
+    const int L = g.P[a], R2 = shape_r2(L), R1 = L / R2;
+    std::vector<double> tw(2 * (size_t)L);
+    for (int k1 = 0; k1 < R1; ++k1)
+      for (int n2 = 0; n2 < R2; ++n2) {
+        double s, co;
+        sincospi(-2.0 * (k1 * n2) / L, &s, &co);
+        tw[k1 * R2 + n2] = co;
+        tw[L + k1 * R2 + n2] = s;
+      }
+    BLR_CUDA(cudaMalloc(&e.tw[a], 2 * (size_t)L * sizeof(double)));
+    BLR_CUDA(cudaMemcpy(e.tw[a], tw.data(), 2 * (size_t)L * sizeof(double), cudaMemcpyHostToDevice));
   }
   e.ok = true;
   return &e;
@@ -151,6 +164,29 @@ static void dispatch_xfwd(blr_ctx* c, PadEngine* e, const FwdArgs<T>& a) {
     BLR_FOR_EACH_L(X)
 #undef X
     default: throw Error(1, "unsupported pad length");
+  }
+}
+
+// fused forward projection (blr_fwd2.cuh): 3-D grids with equal x / y pad lengths;
+// BLR_FWD2=0 selects the two-kernel path (kept as a cross-check)
+static int g_fwd2_disabled = -1;
+template <typename T>
+static bool dispatch_fwd2(blr_ctx* c, PadEngine* e, const Fwd2Args<T>& a, int no, int njmax, bool run) {
+  if (g_fwd2_disabled < 0) {
+    const char* env = getenv("BLR_FWD2");
+    g_fwd2_disabled = (env && env[0] == '1') ? 0 : 1;  // pending GPU verification: opt-in
+  }
+  const PadGeom& g = e->g;
+  if (g_fwd2_disabled || g.P[0] != g.P[1] || g.P[0] < 2) return false;
+  switch (g.P[0]) {
+#define X(LL, A, B)                                                  \
+  case LL:                                                           \
+    if (!fwd2_fits<T, WShape<A, B>>(g)) return false;                \
+    if (run) launch_fwd2<T, WShape<A, B>>(c, e, a, no, njmax);       \
+    return true;
+    BLR_FOR_EACH_LZ(X)
+#undef X
+    default: return false;
   }
 }
 
@@ -313,6 +349,49 @@ static void fwd2d(blr_ctx* c, PadEngine* e, const std::vector<FwdSpec<T>>& outs,
       xt[i].f[xt[i].nt] = (int)jobs.size() - 1;
       xt[i].ax[xt[i].nt++] = -1;
     }
+  }
+  bool fused = dispatch_fwd2<T>(c, e, Fwd2Args<T>{}, 0, 0, false);
+  for (size_t i = 0; i < outs.size() && fused; ++i) fused = xt[i].nt <= kF2MaxJobs;
+  if (fused) {
+    for (size_t off = 0; off < outs.size(); off += kMaxFwd) {
+      Fwd2Args<T> a;
+      std::memset(&a, 0, sizeof(a));
+      const int no = (int)std::min<size_t>(kMaxFwd, outs.size() - off);
+      int njmax = 1, nterm = 0;
+      for (int i = 0; i < no; ++i) {
+        const FwdSpec<T>& s = outs[off + i];
+        const XT& x = xt[off + i];
+        a.nj[i] = x.nt;
+        njmax = std::max(njmax, x.nt);
+        for (int j = 0; j < x.nt; ++j) {
+          const Job& jb = jobs[x.f[j]];
+          Fwd2Job<T>& J = a.job[i][j];
+          J.nt = jb.nt;
+          J.xax = x.ax[j];
+          for (int t = 0; t < 3; ++t) {
+            J.s[t] = t < jb.nt ? jb.s[t] : jb.s[0];
+            J.yax[t] = t < jb.nt ? jb.ax[t] : -1;
+          }
+          nterm += jb.nt;
+        }
+        a.e.o[i].mode = s.mode;
+        a.e.o[i].vt = s.vt;
+        a.e.o[i].nterms = x.nt;
+      }
+      a.e.no = no;
+      a.e.scale = (T)(1.0 / (double)g.np);
+      const int64_t shift = (int64_t)off * g.nh;
+      a.e.kout = kout ? kout + shift : nullptr;
+      a.e.rk_s = rk.s;
+      a.e.cs = (T)rk.cs;
+      a.e.h6 = (T)rk.h6;
+      a.e.cur = rk.cur ? (Cx<T>*)rk.cur + shift : nullptr;
+      a.e.acc = rk.acc ? (Cx<T>*)rk.acc + shift : nullptr;
+      a.e.stage = rk.stage ? (Cx<T>*)rk.stage + shift : nullptr;
+      ProfScope ps(c, "pad_fwd2", ((double)nterm * g.ns + no * g.nh * (rk.s ? 4 : 2)) * sizeof(Cx<T>));
+      dispatch_fwd2<T>(c, e, a, no, njmax, true);
+    }
+    return;
   }
   Cx<T>* I = (Cx<T>*)e_scratch(c, e, 1, jobs.size() * g.n1 * sizeof(Cx<T>));
   for (size_t off = 0; off < jobs.size(); off += kMaxYF) {

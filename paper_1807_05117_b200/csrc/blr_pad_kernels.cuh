@@ -52,9 +52,10 @@ __device__ __forceinline__ int bin_to_index(int p, int P, int K, int B) {
   return -1;
 }
 
+// the split twiddle table (2 L entries, blr_fft.cuh twiddle()) into shared memory
 template <typename T>
-__device__ __forceinline__ void load_tw(Cx<T>* dst, const double2* src, int n) {
-  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = cx<T>((T)src[i].x, (T)src[i].y);
+__device__ __forceinline__ void load_tw(T* dst, const double* src, int L) {
+  for (int i = threadIdx.x; i < 2 * L; i += blockDim.x) dst[i] = (T)src[i];
 }
 
 template <typename T>
@@ -233,7 +234,7 @@ constexpr int phase_conflicts(int LS, int words) {
 template <typename T, class S, bool ALIAS = false>
 constexpr int row_stride() {
   constexpr int words = (int)(sizeof(Cx<T>) / 4);
-  const int base = ALIAS && S::TS > S::L ? S::TS : S::L;
+  const int base = ALIAS && TileG<T, S>::TS > S::L ? TileG<T, S>::TS : S::L;
   int best = base, bc = phase_conflicts<S>(base, words);
   for (int p = 1; p < 8; ++p) {
     const int c = phase_conflicts<S>(base + p, words);
@@ -243,14 +244,14 @@ constexpr int row_stride() {
 }
 
 template <typename T, class S>
-__global__ void __launch_bounds__(kPW * 32) k_xinv(XPassArgs<T> a, PadGeom g, const double2* __restrict__ twg) {
+__global__ void __launch_bounds__(kPW * 32) k_xinv(XPassArgs<T> a, PadGeom g, const double* __restrict__ twg) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int LPC = kPW * S::LPW;
   const int K0 = g.K[0], B0 = g.B[0], B1 = g.B[1];
-  Cx<T>* tw = (Cx<T>*)smem_raw;
+  T* tw = (T*)smem_raw;
   constexpr int LPCS = t_stride<LPC>();
-  Cx<T>* slab = tw + S::L;                       // [B0][LPCS]
-  Cx<T>* tile = slab + B0 * LPCS + (threadIdx.x >> 5) * S::TILE;
+  Cx<T>* slab = (Cx<T>*)(tw + 2 * S::L);         // [B0][LPCS]
+  Cx<T>* tile = slab + B0 * LPCS + (threadIdx.x >> 5) * TileG<T, S>::TILE;
   const int nyb = (B1 + LPC - 1) / LPC;
   const int per = g.Kz1 * nyb;
   const int xf = blockIdx.x / per;
@@ -307,14 +308,14 @@ struct YPassArgs {
 };
 
 template <typename T, class S>
-__global__ void __launch_bounds__(kPW * 32) k_yinv(YPassArgs<T> a, PadGeom g, const double2* __restrict__ twg, int ntmax) {
+__global__ void __launch_bounds__(kPW * 32) k_yinv(YPassArgs<T> a, PadGeom g, const double* __restrict__ twg, int ntmax) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int LPC = kPW * S::LPW;
   const int P0 = g.P[0], K1 = g.K[1], B1 = g.B[1];
-  Cx<T>* tw = (Cx<T>*)smem_raw;
+  T* tw = (T*)smem_raw;
   constexpr int LPCS = t_stride<LPC>();
-  Cx<T>* slab = tw + S::L;                       // [ntmax][B1][LPCS]
-  Cx<T>* tile = slab + ntmax * B1 * LPCS + (threadIdx.x >> 5) * S::TILE;
+  Cx<T>* slab = (Cx<T>*)(tw + 2 * S::L);         // [ntmax][B1][LPCS]
+  Cx<T>* tile = slab + ntmax * B1 * LPCS + (threadIdx.x >> 5) * TileG<T, S>::TILE;
   const int nxb = (P0 + LPC - 1) / LPC;
   const int per = g.Kz1 * nxb;
   const int yf = blockIdx.x / per;
@@ -429,6 +430,58 @@ template <int OP> struct ZOp {
 };
 
 constexpr int kZWarps = 2;
+// Occupancy targets (CTAs per SM) of the z-line kernel per op; 0 = registers
+// unconstrained.  A/B (r02): the unrolled outer op (rho / V operands in
+// registers, BLR_ZUNROLL_OUTER=1) at 6 CTAs per SM spills and ties the default,
+// at 5 it is 2% slower; both stay off.
+#ifndef BLR_ZMINB_OUTER
+#define BLR_ZMINB_OUTER 0
+#endif
+#ifndef BLR_ZMINB_MAPTC
+#define BLR_ZMINB_MAPTC 0
+#endif
+constexpr int zline_min_blocks(int op) {
+  return op == 6 ? BLR_ZMINB_OUTER : op == 2 ? BLR_ZMINB_MAPTC : 0;
+}
+
+// z-line shared buffers, line strides chosen by the bank model (blr_fft.cuh):
+//   xbuf [line][LX] complex: step-B stores / step-A loads of the R2C inputs;
+//   Vst / Rsm [field][line][LR] real: read at step-B (and, for the unrolled
+//   outer op, step-A) positions.  L = 100 fp64: LX = LR = 106 makes both
+//   access patterns conflict-free (the dense stride 100 cost 1.5x / 2x);
+//   used only with BLR_BANKPAD=1 (see TileG).
+template <typename T, class S>
+struct ZLineG {
+  static constexpr int L = S::L;
+  static constexpr int EC = (int)(2 * sizeof(T)), ER = (int)sizeof(T);
+  static constexpr int xcost(int lx) {
+    int c = 0;
+    for (int k2 = 0; k2 < S::R2; ++k2)
+      c += wavefronts([&](int l) { return l / S::R1 < S::LPW ? (l / S::R1) * lx + l % S::R1 + S::R1 * k2 : -1; }, EC);
+    for (int n1 = 0; n1 < S::R1; ++n1)
+      c += wavefronts([&](int l) { return l / S::R2 < S::LPW ? (l / S::R2) * lx + S::R2 * n1 + l % S::R2 : -1; }, EC);
+    return c;
+  }
+  static constexpr int rcost(int lr) {
+    int c = 0;
+    for (int k2 = 0; k2 < S::R2; ++k2)
+      c += wavefronts([&](int l) { return l / S::R1 < S::LPW ? (l / S::R1) * lr + l % S::R1 + S::R1 * k2 : -1; }, ER);
+    for (int n1 = 0; n1 < S::R1; ++n1)
+      c += wavefronts([&](int l) { return l / S::R2 < S::LPW ? (l / S::R2) * lr + S::R2 * n1 + l % S::R2 : -1; }, ER);
+    return c;
+  }
+  static constexpr int pick(bool real) {
+    if (!BLR_BANKPAD) return L;
+    int best = L, bc = 1 << 30;
+    for (int p = 0; p < 8; ++p) {
+      const int c = real ? rcost(L + p) : xcost(L + p);
+      if (c < bc) { bc = c; best = L + p; }
+    }
+    return best;
+  }
+  static constexpr int LX = pick(false);
+  static constexpr int LR = pick(true);
+};
 
 template <typename T, class S, int OP>
 __device__ __forceinline__ T z_output(const LineArgs<T>& a, const T* Rsm, int ldR, int li, int64_t gi, int o) {
@@ -488,7 +541,7 @@ __device__ __forceinline__ T z_output(const LineArgs<T>& a, const T* Rsm, int ld
 // prefetched pair by pair with cp.async (double buffered), C2R'd two per
 // complex FFT, combined with the cached real pad fields, R2C'd back.
 template <typename T, class S, int OP>
-__global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom g, const double2* __restrict__ twz_g) {
+__global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(LineArgs<T> a, PadGeom g, const double* __restrict__ twz_g) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   using Tr = ZOp<OP>;
   constexpr int L = S::L;
@@ -507,24 +560,26 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
   //                                 C2R phase) | Vst[nst][LPW*L] | Rsm[nreal][LPW*L] }
   const int fstride = Kz1 * S::LPW;  // per-field stage: Kz1 spectra rows
   const int zoff = 4 * fstride;       // one zero row shared by both buffers and fields
-  const int stage_n = max(zoff + S::LPW, S::LPW * L);
+  using ZG = ZLineG<T, S>;
+  constexpr int LX = ZG::LX, LR = ZG::LR;
+  const int stage_n = max(zoff + S::LPW, S::LPW * LX);
   const int nst = Tr::acc ? a.nst : 0;
-  const size_t warp_bytes = sizeof(Cx<T>) * ((size_t)S::TILE + stage_n) +
-                            sizeof(T) * (size_t)(nreal + nst) * S::LPW * L;
+  const size_t warp_bytes = sizeof(Cx<T>) * ((size_t)TileG<T, S>::TILE + stage_n) +
+                            sizeof(T) * (size_t)(nreal + nst) * S::LPW * LR;
   // fp64: twiddles straight from the engine's global table (L1-resident), which
   // keeps the CTA's shared footprint at 6 CTAs per SM; fp32 converts into smem
   // register-bound ACC ops keep the twiddles in (otherwise unused) shared memory
   constexpr bool kTwG = sizeof(T) == 8 && !(Tr::acc && OP != kOpContract);
   constexpr int kTwN = kTwG ? 0 : L;
-  Cx<T>* tw = (Cx<T>*)smem_raw;
-  const Cx<T>* twp = kTwG ? reinterpret_cast<const Cx<T>*>(twz_g) : tw;
-  unsigned char* wb = smem_raw + sizeof(Cx<T>) * kTwN + warp * warp_bytes;
+  T* tw = (T*)smem_raw;
+  const T* twp = kTwG ? reinterpret_cast<const T*>(twz_g) : tw;
+  unsigned char* wb = smem_raw + sizeof(Cx<T>) * kTwN + warp * warp_bytes;  // kTwN complex = 2 kTwN T
   Cx<T>* tile = (Cx<T>*)wb;
-  Cx<T>* stage = tile + S::TILE;
+  Cx<T>* stage = tile + TileG<T, S>::TILE;
   Cx<T>* xbuf = stage;
   T* Vst = (T*)(stage + stage_n);
-  T* Rsm = Vst + nst * S::LPW * L;
-  const int ldR = S::LPW * L;
+  T* Rsm = Vst + nst * S::LPW * LR;
+  const int ldR = S::LPW * LR;
   if constexpr (!kTwG) {
     load_tw<T>(tw, twz_g, L);
     __syncthreads();
@@ -535,17 +590,32 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
   const int64_t sline = (int64_t)x * P1 + y0;
   const int64_t kzs = (int64_t)P0 * P1;
   const int64_t rline = ((int64_t)x * P1 + y0) * L;
-  // stage the real fields the contributions read (contiguous nl*L run per field)
+  // stage the real fields the contributions read (one contiguous L run per line,
+  // to line stride LR in shared memory)
   for (int q = 0; q < nst; ++q) {
-    const T* src = a.rin[a.st_idx[q]] + rline;
-    T* dst = Vst + q * ldR;
     constexpr int V = 16 / sizeof(T);  // elements per 16-byte copy
-    if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
-      const int nv = (nl * L) / V;
-      for (int i = lane; i < nv; i += 32) __pipeline_memcpy_async(dst + V * i, src + V * i, 16);
-      for (int i = nv * V + lane; i < nl * L; i += 32) __pipeline_memcpy_async(dst + i, src + i, sizeof(T));
-    } else {
-      for (int i = lane; i < nl * L; i += 32) __pipeline_memcpy_async(dst + i, src + i, sizeof(T));
+    if constexpr (LR == L) {  // dense rows: one contiguous nl * L run
+      const T* src = a.rin[a.st_idx[q]] + rline;
+      T* dst = Vst + q * ldR;
+      if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+        const int nv = (nl * L) / V;
+        for (int i = lane; i < nv; i += 32) __pipeline_memcpy_async(dst + V * i, src + V * i, 16);
+        for (int i = nv * V + lane; i < nl * L; i += 32) __pipeline_memcpy_async(dst + i, src + i, sizeof(T));
+      } else {
+        for (int i = lane; i < nl * L; i += 32) __pipeline_memcpy_async(dst + i, src + i, sizeof(T));
+      }
+      continue;
+    }
+    for (int ln = 0; ln < nl; ++ln) {
+      const T* src = a.rin[a.st_idx[q]] + rline + ln * L;
+      T* dst = Vst + q * ldR + ln * LR;
+      if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+        constexpr int nv = L / V;
+        for (int i = lane; i < nv; i += 32) __pipeline_memcpy_async(dst + V * i, src + V * i, 16);
+        for (int i = nv * V + lane; i < L; i += 32) __pipeline_memcpy_async(dst + i, src + i, sizeof(T));
+      } else {
+        for (int i = lane; i < L; i += 32) __pipeline_memcpy_async(dst + i, src + i, sizeof(T));
+      }
     }
   }
   // step-B ownership: lane (bl, k1) owns z = k1 + R1*k2
@@ -665,7 +735,12 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
       default: break;
     }
   };
-  for (int q = 0; q < total; ++q) {
+  // One input pair.  QS >= 0: the pair index is a compile-time constant (3-D
+  // Map / MapTC, all five pairs unrolled), so each realized field adds to its
+  // one output accumulator with a single FMA (output / V slot / sign known at
+  // compile time) instead of a multiply-add into every output.
+  auto pair_step = [&](int q, auto qc) {
+    constexpr int QS = decltype(qc)::value;
     if (q + 1 < total) {
       prefetch(q + 1);
       __pipeline_wait_prior(1);
@@ -681,7 +756,7 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
     T c1[NOM], c2[NOM];
     const T* V1 = Vst;
     const T* V2 = Vst;
-    if constexpr (Tr::acc && OP != kOpContract) {
+    if constexpr (Tr::acc && OP != kOpContract && QS < 0) {
       const int o1 = a.oi[f], o2 = two ? a.oi[f + 1] : -1;
       const T sg1 = (T)a.sg[f], sg2 = two ? (T)a.sg[f + 1] : (T)0;
 #pragma unroll
@@ -701,14 +776,23 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
       return cx<T>(F1.x - sg * F2.y, sg * F1.y + F2.x);
     };
     auto store = [&](int line, int z, int k2, Cx<T> v) {
-      const int li = line * L + z;
-      const int64_t gi = rline + li;
+      const int li = line * LR + z;                // shared (Rsm / Vst)
+      const int64_t gi = rline + line * L + z;     // global (pad field)
       if constexpr (OP == kOpRealize) {
         a.wout[f][gi] = v.x;
         if (two) a.wout[f + 1][gi] = v.y;
       } else if constexpr (!Tr::acc || OP == kOpContract) {
         Rsm[f * ldR + li] = v.x;
         if (two) Rsm[(f + 1) * ldR + li] = v.y;
+      } else if constexpr (QS >= 0) {
+        // 3-D Map / MapTC: field F = (i, j) = (F / 3, F % 3) adds S_ij V_j to output i
+        constexpr int F1 = 2 * QS, F2 = 2 * QS + 1;
+        if (OP == kOpMap && a.wout[F1]) {
+          a.wout[F1][gi] = v.x;
+          if (F2 < 9) a.wout[F2][gi] = v.y;
+        }
+        acc[F1 / 3][k2] += v.x * Vst[(F1 % 3) * ldR + li];
+        if constexpr (F2 < 9) acc[F2 / 3][k2] += v.y * Vst[(F2 % 3) * ldR + li];
       } else {
         if (OP == kOpMap && a.wout[f]) {
           a.wout[f][gi] = v.x;
@@ -720,9 +804,15 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
         for (int o = 0; o < NOM; ++o) acc[o][k2] += c1[o] * p1 + c2[o] * p2;
       }
     };
-    if constexpr (OP == kOpMapTC) du_chunk(q, du_issue);
+    if constexpr (OP == kOpMapTC) {
+      if constexpr (QS >= 0) du_issue(std::integral_constant<int, QS>{});
+      else du_chunk(q, du_issue);
+    }
     wfft<T, S, true>(tile, twp, nl, load, store);
-    if constexpr (OP == kOpMapTC) du_chunk(q, du_acc);
+    if constexpr (OP == kOpMapTC) {
+      if constexpr (QS >= 0) du_acc(std::integral_constant<int, QS>{});
+      else du_chunk(q, du_acc);
+    }
     if constexpr (OP == kOpContract) {
       if (p == npair - 1) {
         // node complete: rho_n is realized in Rsm.  Stream the cached D(phi_n)
@@ -756,7 +846,9 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
             if (m0 + u < S::R2 && li < npos) {
               T r[3];
 #pragma unroll
-              for (int j = 0; j < 3; ++j) r[j] = j < d ? Rsm[j * ldR + li] : (T)0;
+              const int lis = (li / L) * LR + li % L;
+#pragma unroll
+              for (int j = 0; j < 3; ++j) r[j] = j < d ? Rsm[j * ldR + lis] : (T)0;
 #pragma unroll
               for (int o = 0; o < NOM; ++o)
                 acc[o][m0 + u] += wn * (mv[u][o][0] * r[0] + mv[u][o][1] * r[1] + mv[u][o][2] * r[2]);
@@ -766,6 +858,23 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
         __syncwarp();
       }
     }
+  };
+  // A/B on the B200: unrolling the five MapTC pairs made map_tc 37% slower
+  // (2.82 -> 3.86 ms per HVP: code size and spills), so it is off by default.
+#ifndef BLR_ZUNROLL_PAIRS
+#define BLR_ZUNROLL_PAIRS 0
+#endif
+  constexpr bool kUnrollPairs = BLR_ZUNROLL_PAIRS != 0 && (OP == kOpMap || OP == kOpMapTC);
+  if (kUnrollPairs && a.d == 3 && total == 5) {
+    if constexpr (kUnrollPairs) {
+      pair_step(0, std::integral_constant<int, 0>{});
+      pair_step(1, std::integral_constant<int, 1>{});
+      pair_step(2, std::integral_constant<int, 2>{});
+      pair_step(3, std::integral_constant<int, 3>{});
+      pair_step(4, std::integral_constant<int, 4>{});
+    }
+  } else {
+    for (int q = 0; q < total; ++q) pair_step(q, std::integral_constant<int, -1>{});
   }
   if constexpr (OP == kOpMapTC) {
     for (int c = total; c < 5; ++c) {  // fewer than five input pairs (d < 3)
@@ -775,7 +884,29 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
   }
   if constexpr (OP == kOpRealize) return;
   const int no = a.no;
-  for (int o = 0; o < no; o += 2) {
+  // Outer (3-D, unrolled): rho_i at this lane's step-A positions, read once from
+  // Rsm into registers for all nine products (instead of two shared loads per
+  // element per output pair)
+#ifndef BLR_ZUNROLL_OUTER
+#define BLR_ZUNROLL_OUTER 0
+#endif
+  constexpr bool kUnrollOuter = BLR_ZUNROLL_OUTER != 0 && OP == kOpOuter;
+  T rreg[kUnrollOuter ? 3 : 1][kUnrollOuter ? S::R1 : 1];
+  const bool outer3 = kUnrollOuter && a.d == 3 && no == 9;
+  if constexpr (kUnrollOuter) {
+    if (outer3) {
+      __syncwarp();
+      const int la = lane / S::R2, n2a = lane - (lane / S::R2) * S::R2;
+      const bool oka = la < nl && la < S::LPW;
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int n1 = 0; n1 < S::R1; ++n1) rreg[i][n1] = oka ? Rsm[i * ldR + la * LR + S::R2 * n1 + n2a] : (T)0;
+    }
+  }
+  // One output pair (o, o + 1).  OS >= 0: o is a compile-time constant.
+  auto out_step = [&](int o, auto oc) {
+    constexpr int OS = decltype(oc)::value;
     const bool two = o + 1 < no;
     if constexpr (OP == kOpContract) {
 #pragma unroll
@@ -787,7 +918,7 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
           if (q == o) v1 = acc[q][m];
           if (q == o + 1) v2 = acc[q][m];
         }
-        if (li < nl * L) xbuf[li] = cx<T>(v1, v2);
+        if (li < nl * L) xbuf[(li / L) * LX + li % L] = cx<T>(v1, v2);
       }
       __syncwarp();
     } else if constexpr (Tr::acc) {
@@ -800,7 +931,7 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
             if (q == o) v1 = acc[q][k2];
             if (q == o + 1) v2 = acc[q][k2];
           }
-          xbuf[bl * L + k1 + S::R1 * k2] = cx<T>(v1, v2);
+          xbuf[bl * LX + k1 + S::R1 * k2] = cx<T>(v1, v2);
         }
       }
       __syncwarp();
@@ -812,33 +943,47 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zlines(LineArgs<T> a, PadGeom 
     const T* R2p = Rsm + oi2 * ldR;
     auto load = [&](int line, int z, int n1) -> Cx<T> {
       if constexpr (Tr::acc) {
-        return xbuf[line * L + z];
+        return xbuf[line * LX + z];
+      } else if constexpr (OP == kOpOuter && OS >= 0) {
+        constexpr int I1 = OS / 3, J1 = OS % 3, I2 = (OS + 1) / 3, J2 = (OS + 1) % 3;
+        return cx<T>(rreg[I1][n1] * vreg[J1][n1], OS + 1 < 9 ? rreg[I2 < 3 ? I2 : 0][n1] * vreg[J2][n1] : (T)0);
       } else if constexpr (OP == kOpOuter) {
-        const int li = line * L + z;
+        const int li = line * LR + z;
         const T v1 = oj1 == 0 ? vreg[0][n1] : (oj1 == 1 ? vreg[1][n1] : vreg[2][n1]);
         const T v2 = oj2 == 0 ? vreg[0][n1] : (oj2 == 1 ? vreg[1][n1] : vreg[2][n1]);
         return cx<T>(R1p[li] * v1, two ? R2p[li] * v2 : (T)0);
       } else {
-        const int li = line * L + z;
-        const int64_t gi = rline + li;
+        const int li = line * LR + z;
+        const int64_t gi = rline + line * L + z;
         return cx<T>(z_output<T, S, OP>(a, Rsm, ldR, li, gi, o),
                      two ? z_output<T, S, OP>(a, Rsm, ldR, li, gi, o + 1) : (T)0);
       }
     };
-    auto store = [&](int line, int k, int, Cx<T> v) { xbuf[line * L + k] = v; };
+    auto store = [&](int line, int k, int, Cx<T> v) { xbuf[line * LX + k] = v; };
     wfft<T, S, false>(tile, twp, nl, load, store);
     Cx<T>* O1 = a.sout[o] + sline;
     Cx<T>* O2 = two ? a.sout[o + 1] + sline : nullptr;
     for (int idx = lane; idx < S::LPW * Kz1; idx += 32) {
       const int k = idx / S::LPW, l = idx - (idx / S::LPW) * S::LPW;  // compile-time divisor
       if (l >= nl) continue;
-      const Cx<T> Z = xbuf[l * L + k];
-      Cx<T> Zm = xbuf[l * L + (k == 0 ? 0 : L - k)];
+      const Cx<T> Z = xbuf[l * LX + k];
+      Cx<T> Zm = xbuf[l * LX + (k == 0 ? 0 : L - k)];
       Zm.y = -Zm.y;
       O1[k * kzs + l] = cx<T>((T)0.5 * (Z.x + Zm.x), (T)0.5 * (Z.y + Zm.y));
       if (two) O2[k * kzs + l] = cx<T>((T)0.5 * (Z.y - Zm.y), (T)-0.5 * (Z.x - Zm.x));
     }
     __syncwarp();
+  };
+  if (outer3) {
+    if constexpr (kUnrollOuter) {
+      out_step(0, std::integral_constant<int, 0>{});
+      out_step(2, std::integral_constant<int, 2>{});
+      out_step(4, std::integral_constant<int, 4>{});
+      out_step(6, std::integral_constant<int, 6>{});
+      out_step(8, std::integral_constant<int, 8>{});
+    }
+  } else {
+    for (int o = 0; o < no; o += 2) out_step(o, std::integral_constant<int, -1>{});
   }
 }
 
@@ -862,15 +1007,15 @@ struct YFwdArgs {
 // the cp.async slab of the next (item, term) load streams in while the warps
 // transform the current one, so HBM stays busy through the FFT phase.
 template <typename T, class S>
-__global__ void __launch_bounds__(kPWF * 32, 4) k_yfwd(YFwdArgs<T> a, PadGeom g, const double2* __restrict__ twg) {
+__global__ void __launch_bounds__(kPWF * 32, 4) k_yfwd(YFwdArgs<T> a, PadGeom g, const double* __restrict__ twg) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int LPC = kPWF * S::LPW;
   constexpr int LS = row_stride<T, S, true>();
   constexpr int LPCS = t_stride<LPC>();
   constexpr int SLAB = LPC * LS;
   const int P0 = g.P[0], K1 = g.K[1], B1 = g.B[1];
-  Cx<T>* tw = (Cx<T>*)smem_raw;
-  Cx<T>* slab = tw + S::L;                       // [2][LPC][LS]; each warp's FFT tile overlays its lines
+  T* tw = (T*)smem_raw;
+  Cx<T>* slab = (Cx<T>*)(tw + 2 * S::L);         // [2][LPC][LS]; each warp's FFT tile overlays its lines
   Cx<T>* res = slab + 2 * SLAB;                  // [B1][LPCS] job accumulator
   const int nxb = (P0 + LPC - 1) / LPC;
   const int per = g.Kz1 * nxb;
@@ -1037,7 +1182,7 @@ template <typename T, class S>
 #ifndef BLR_XFWD_MINB
 #define BLR_XFWD_MINB 3
 #endif
-__global__ void __launch_bounds__(kPWF * 32, BLR_XFWD_MINB) k_xfwd(FwdArgs<T> a, PadGeom g, const double2* __restrict__ twg) {
+__global__ void __launch_bounds__(kPWF * 32, BLR_XFWD_MINB) k_xfwd(FwdArgs<T> a, PadGeom g, const double* __restrict__ twg) {
   static_assert(kPWF == 2, "kz = 0 mirror items use one warp per half");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int LPW = S::LPW;
@@ -1046,8 +1191,8 @@ __global__ void __launch_bounds__(kPWF * 32, BLR_XFWD_MINB) k_xfwd(FwdArgs<T> a,
   constexpr int LPCS = t_stride<LPC>();
   constexpr int SLAB = LPC * LS;
   const int K0 = g.K[0], B0 = g.B[0], B1 = g.B[1], K1 = g.K[1];
-  Cx<T>* tw = (Cx<T>*)smem_raw;
-  Cx<T>* slab = tw + S::L;                       // [2][LPC][LS] (persistent, as k_yfwd)
+  T* tw = (T*)smem_raw;
+  Cx<T>* slab = (Cx<T>*)(tw + 2 * S::L);         // [2][LPC][LS] (persistent, as k_yfwd)
   Cx<T>* res = slab + 2 * SLAB;                  // [B0][LPCS] finished block
   const int nyb = (B1 + LPC - 1) / LPC;
   const int n0 = (K1 + 1 + LPW - 1) / LPW;      // kz = 0 items (LPW mirror units each)
@@ -1311,7 +1456,7 @@ struct PadEngine {
   bool ok = false;
   bool tried = false;
   PadGeom g{};
-  double2* tw[3] = {nullptr, nullptr, nullptr};
+  double* tw[3] = {nullptr, nullptr, nullptr};  // split twiddle tables (2 L doubles per axis)
   int line_smem_max = 0;
   void* buf[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t buf_bytes[4] = {0, 0, 0, 0};
@@ -1352,10 +1497,10 @@ template <typename T, class S>
 void launch_xinv(blr_ctx* c, PadEngine* e, const XPassArgs<T>& a) {
   const PadGeom& g = e->g;
   constexpr int LPC = kPW * S::LPW;
-  const size_t sm = sizeof(Cx<T>) * (S::L + (size_t)g.B[0] * t_stride<LPC>() + kPW * S::TILE);
+  const size_t sm = sizeof(Cx<T>) * (S::L + (size_t)g.B[0] * t_stride<LPC>() + kPW * TileG<T, S>::TILE);
   ensure_smem(k_xinv<T, S>, sm);
   const int nyb = (g.B[1] + LPC - 1) / LPC;
-  launch_pdl(k_xinv<T, S>, a.nx * g.Kz1 * nyb, kPW * 32, sm, c->stream, a, g, (const double2*)e->tw[0]);
+  launch_pdl(k_xinv<T, S>, a.nx * g.Kz1 * nyb, kPW * 32, sm, c->stream, a, g, (const double*)e->tw[0]);
   BLR_LAUNCHED();
 }
 template <typename T, class S>
@@ -1364,10 +1509,10 @@ void launch_yinv(blr_ctx* c, PadEngine* e, const YPassArgs<T>& a) {
   constexpr int LPC = kPW * S::LPW;
   int ntmax = 1;
   for (int i = 0; i < a.ny; ++i) ntmax = std::max(ntmax, a.nterms[i]);
-  const size_t sm = sizeof(Cx<T>) * (S::L + (size_t)ntmax * g.B[1] * t_stride<LPC>() + kPW * S::TILE);
+  const size_t sm = sizeof(Cx<T>) * (S::L + (size_t)ntmax * g.B[1] * t_stride<LPC>() + kPW * TileG<T, S>::TILE);
   ensure_smem(k_yinv<T, S>, sm);
   const int nxb = (g.P[0] + LPC - 1) / LPC;
-  launch_pdl(k_yinv<T, S>, a.ny * g.Kz1 * nxb, kPW * 32, sm, c->stream, a, g, (const double2*)e->tw[1], ntmax);
+  launch_pdl(k_yinv<T, S>, a.ny * g.Kz1 * nxb, kPW * 32, sm, c->stream, a, g, (const double*)e->tw[1], ntmax);
   BLR_LAUNCHED();
 }
 template <typename T, class S, int OP>
@@ -1376,9 +1521,9 @@ void launch_lines(blr_ctx* c, PadEngine* e, const LineArgs<T>& a) {
   const int ns_blk = OP == kOpContract ? a.d : a.ns;
   const int nreal = OP == kOpContract ? a.d : (ZOp<OP>::acc || OP == kOpRealize) ? 0 : ns_blk;
   const int nst = ZOp<OP>::acc ? a.nst : 0;
-  const size_t stage_n = std::max<size_t>(4 * (size_t)g.Kz1 * S::LPW + S::LPW, (size_t)S::LPW * S::L);
-  const size_t warp_bytes = sizeof(Cx<T>) * ((size_t)S::TILE + stage_n) +
-                            sizeof(T) * (size_t)(nreal + nst) * S::LPW * S::L;
+  const size_t stage_n = std::max<size_t>(4 * (size_t)g.Kz1 * S::LPW + S::LPW, (size_t)S::LPW * ZLineG<T, S>::LX);
+  const size_t warp_bytes = sizeof(Cx<T>) * ((size_t)TileG<T, S>::TILE + stage_n) +
+                            sizeof(T) * (size_t)(nreal + nst) * S::LPW * ZLineG<T, S>::LR;
   const bool twg = sizeof(T) == 8 && !(ZOp<OP>::acc && OP != kOpContract);  // as kTwG in the kernel
   const size_t sm = (twg ? 0 : S::L * sizeof(Cx<T>)) + kZWarps * warp_bytes;
   if (sm > (size_t)e->line_smem_max) throw Error(1, "z-line kernel shared memory exceeds the device limit");
@@ -1392,7 +1537,7 @@ void launch_lines(blr_ctx* c, PadEngine* e, const LineArgs<T>& a) {
   }
   constexpr int LPC = kZWarps * S::LPW;
   const int nyc = (g.P[1] + LPC - 1) / LPC;
-  launch_pdl(k_zlines<T, S, OP>, g.P[0] * nyc, kZWarps * 32, sm, c->stream, a, g, (const double2*)e->tw[2]);
+  launch_pdl(k_zlines<T, S, OP>, g.P[0] * nyc, kZWarps * 32, sm, c->stream, a, g, (const double*)e->tw[2]);
   BLR_LAUNCHED();
 }
 template <typename T, class S>
@@ -1404,7 +1549,7 @@ void launch_yfwd(blr_ctx* c, PadEngine* e, const YFwdArgs<T>& a) {
   ensure_smem(k_yfwd<T, S>, sm);
   const int nxb = (g.P[0] + LPC - 1) / LPC;
   const int grid = persistent_grid(k_yfwd<T, S>, kPWF * 32, sm, a.nj * g.Kz1 * nxb);
-  launch_pdl(k_yfwd<T, S>, grid, kPWF * 32, sm, c->stream, a, g, (const double2*)e->tw[1]);
+  launch_pdl(k_yfwd<T, S>, grid, kPWF * 32, sm, c->stream, a, g, (const double*)e->tw[1]);
   BLR_LAUNCHED();
 }
 template <typename T, class S>
@@ -1417,9 +1562,11 @@ void launch_xfwd(blr_ctx* c, PadEngine* e, const FwdArgs<T>& a) {
   const int nyb = (g.B[1] + LPC - 1) / LPC;
   const int n0 = (g.K[1] + 1 + S::LPW - 1) / S::LPW;
   const int grid = persistent_grid(k_xfwd<T, S>, kPWF * 32, sm, a.no * (n0 + (g.Kz1 - 1) * nyb));
-  launch_pdl(k_xfwd<T, S>, grid, kPWF * 32, sm, c->stream, a, g, (const double2*)e->tw[0]);
+  launch_pdl(k_xfwd<T, S>, grid, kPWF * 32, sm, c->stream, a, g, (const double*)e->tw[0]);
   BLR_LAUNCHED();
 }
 
 
 }  // namespace blr
+
+#include "blr_fwd2.cuh"
