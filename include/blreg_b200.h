@@ -55,6 +55,10 @@ int blr_version(void);
  * RK4 updates, warps, ...).  Off by default; when on, every instrumented launch
  * records events on its stream.  report: JSON {"name": [launches, total_ms,
  * algorithmic_bytes], ...} of everything recorded since the last report. */
+/* engine option: 1 fused y+x forward projection (one thread-block cluster
+ * per (output, kz) plane), 0 (default) the two-kernel path; both give
+ * bit-identical results (tests/test_gpu_fused.py) */
+int blr_set_fused_forward(int on);
 int blr_profile_enable(int on);
 int blr_profile_report(char* buf, int64_t len);
 

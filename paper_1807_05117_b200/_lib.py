@@ -29,6 +29,7 @@ SIGNATURES = {
     "blr_launch_count": [],
     "blr_version": [],
     "blr_profile_enable": [_i],
+    "blr_set_fused_forward": [_i],
     "blr_profile_report": [C.c_char_p, _i64],
     "blr_include": [_vp, _i, _vp, _i, _ip, _vp],
     "blr_project": [_vp, _i, _vp, _i, _vp],

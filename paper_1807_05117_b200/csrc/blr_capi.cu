@@ -63,6 +63,10 @@ const char* blr_last_error(void) { return g_err.c_str(); }
 int64_t blr_launch_count(void) { return launch_count(); }
 int blr_version(void) { return 1; }
 
+int blr_set_fused_forward(int on) {
+  return guarded([&] { set_fused_forward(on); });
+}
+
 int blr_profile_enable(int on) {
   return guarded([&] { profile_enable(on != 0); });
 }

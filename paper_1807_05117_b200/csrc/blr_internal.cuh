@@ -88,6 +88,7 @@ template <typename T> void conv_matvec(blr_ctx* c, const Cx<T>* M, const Cx<T>* 
 // fused pad engine (blr_pad.cu); each returns false when unavailable (v1 fallback)
 template <typename T> bool pad_engine_ok(blr_ctx* c);
 void pad_engine_release(blr_ctx* c);
+void set_fused_forward(int on);
 template <typename T> bool forward_map_v2(blr_ctx* c, FlowRef v, int substeps, Cx<T>* phi, T* du_cache);
 template <typename T> bool inverse_map_and_volume_v2(blr_ctx* c, FlowRef v, int substeps, Cx<T>* psi, Cx<T>* vol);
 template <typename T> bool state_tangents_v2(blr_ctx* c, FlowRef v, FlowRef dv, int substeps, int flags,

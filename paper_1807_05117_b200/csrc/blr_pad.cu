@@ -167,14 +167,19 @@ static void dispatch_xfwd(blr_ctx* c, PadEngine* e, const FwdArgs<T>& a) {
   }
 }
 
-// fused forward projection (blr_fwd2.cuh): 3-D grids with equal x / y pad lengths;
-// BLR_FWD2=0 selects the two-kernel path (kept as a cross-check)
+// fused forward projection (blr_fwd2.cuh): 3-D grids with equal x / y pad lengths.
+// Opt-in (BLR_FWD2=1 or blr_set_fused_forward(1)): bit-identical to the
+// two-kernel path, but A/B on the B200 (r02, 128^3 / K=32) it ties it for
+// one-job outputs (state GN HVP 5.59 vs 5.43 ms) and loses for the flux
+// divergence (2 jobs, 93 KB smem -> 2 CTAs/SM: deformation 11.4 vs 9.76 ms);
+// ncu: exposed bulk-load and cluster-barrier waits (no double buffering).
 static int g_fwd2_disabled = -1;
+void set_fused_forward(int on) { g_fwd2_disabled = on ? 0 : 1; }
 template <typename T>
 static bool dispatch_fwd2(blr_ctx* c, PadEngine* e, const Fwd2Args<T>& a, int no, int njmax, bool run) {
   if (g_fwd2_disabled < 0) {
     const char* env = getenv("BLR_FWD2");
-    g_fwd2_disabled = (env && env[0] == '1') ? 0 : 1;  // pending GPU verification: opt-in
+    g_fwd2_disabled = (env && env[0] == '1') ? 0 : 1;
   }
   const PadGeom& g = e->g;
   if (g_fwd2_disabled || g.P[0] != g.P[1] || g.P[0] < 2) return false;

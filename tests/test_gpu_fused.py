@@ -72,3 +72,32 @@ def test_momentum_contract_rejects_missing_weights():
     with pytest.raises(ValueError, match="bad arguments"):
         _lib.call("blr_momentum_contract", dom.ctx().bind(), ptr(v.values), v.n_stored, v.n_steps, 1,
                   ptr(rho_end), None, None, 0, None, 0, ptr(out))
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("kind", ["def", "state"])
+@pytest.mark.parametrize("N,K", [(128, 32), (64, 16), (40, 12)])
+def test_fused_forward_projection_bit_identical(dtype, kind, N, K):
+    """The fused y+x forward projection (blr_fwd2.cuh: one cluster per
+    (output, kz) plane, DSMEM exchange, kz = 0 mirror symmetrization) performs
+    the two-kernel path's arithmetic operation for operation: energy, gradient
+    and GN / Newton HVPs must be bit-identical with it on and off."""
+    dom = B.Domain((N,) * 3, (K,) * 3, alpha=0.02, order=2, dtype=dtype)
+    rng = np.random.default_rng(11)
+    I0, I1 = bench.band_image(dom, rng), bench.band_image(dom, rng)
+    v = B.TimeFlow(dom, bench.smooth_vector_block(dom, rng, 0.5 / N, 2.0)[None], 4, True)
+    w = B.TimeFlow(dom, bench.smooth_vector_block(dom, rng, 0.5 / N, 2.0)[None], 4, True)
+    cls = B.DeformationObjective if kind == "def" else B.StateObjective
+    out = {}
+    try:
+        for on in (0, 1):
+            _lib.call("blr_set_fused_forward", on)
+            obj = cls(dom, I0, I1, B.ProblemConfig(sigma2=0.1, n_time_steps=4))
+            ev = obj.gradient(v)
+            out[on] = (ev.energy, ev.gradient.values.clone(), ev.hessian_vector(w, True).values.clone(),
+                       ev.hessian_vector(w, False).values.clone())
+    finally:
+        _lib.call("blr_set_fused_forward", 0)
+    assert out[0][0] == out[1][0]
+    for a, b in zip(out[0][1:], out[1][1:]):
+        assert torch.equal(a, b)
