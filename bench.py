@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--registration", type=int, default=1, help="also time one full GN registration")
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--profile-only", action="store_true", help="one instrumented HVP, no timing")
+    ap.add_argument("--in-flight", type=int, default=2,
+                    help="--batch: pairs registered concurrently per GPU (threads + streams)")
     ap.add_argument("--batch", type=int, default=0,
                     help="SURVEY config 5: register this many seeded pairs sharded over the ranks "
                          "(NCCL atlas all_reduce + stats all_gather) and report pairs/s instead of HVP/s")
@@ -678,7 +680,7 @@ def run_batch(args, rank, world, local):
     barrier(world)
     t0 = time.perf_counter()
     res = Bt.register_batch(pair, n_pairs=args.batch, domain=dom, problem=problem, solver_cfg=cfg,
-                            objective=args.objective)
+                            objective=args.objective, in_flight=args.in_flight)
     torch.cuda.synchronize()
     wall = max_over_ranks(time.perf_counter() - t0, world)
     if rank == 0:
@@ -690,7 +692,8 @@ def run_batch(args, rank, world, local):
                 "data": "synthetic (blob_pair seeds 1..P: 6 periodic bumps, cubic-warped target)",
                 "config": {**workload(args), "workload": f"batch_{args.batch}x_{args.objective}_registration",
                            "sigma2": 0.03, "alpha": 0.01, "solver": "SolverConfig() defaults (GN, 10 inner)",
-                           "pairs": args.batch, "parallelism": f"pairs round-robin over {world} ranks"},
+                           "pairs": args.batch, "in_flight_per_gpu": args.in_flight,
+                           "parallelism": f"pairs round-robin over {world} ranks, {args.in_flight} in flight per GPU"},
                 "batch": {"pcg_total_mean": float(st[:, Bt.STATS.index("pcg_total")].mean()),
                           "outer_mean": float(st[:, Bt.STATS.index("outer")].mean()),
                           "converged": int((st[:, Bt.STATS.index("status")] == 0).sum()),

@@ -12,11 +12,20 @@ collectives finish the batch:
   average (one image, 16.8 MB at 128^3 fp64);
 * ``all_gather`` of a fixed-size float64 stats table (energy, MSE_rel,
   grad_rel, PCG total, Jacobian extrema, wall time, status, outer iterations).
+
+Within a rank, ``in_flight`` > 1 registers that many pairs concurrently, each
+on its own host thread and torch stream (the boundary gives every (thread,
+stream) pair its own device context, ``domain.py`` ``Context``): one
+registration's kernels keep only 8-24 warps per SM busy, so independent pairs
+fill the GPU.  Results and the atlas sum are combined in pair order, so they
+do not depend on ``in_flight``.
 """
 
 from __future__ import annotations
 
+import threading
 import time
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 from typing import Callable, Sequence
 
@@ -66,7 +75,7 @@ def register_pair_fn(domain, problem, solver_cfg, objective: str = "deformation"
         res = minimize(obj, TimeFlow.zero(domain, problem.n_time_steps), solver_cfg)
         jd = gridops.jacobian_determinant(
             domain, spectral.include(domain, res.evaluation.cache.forward[-1], check=False))
-        torch.cuda.synchronize()
+        torch.cuda.current_stream().synchronize()
         row = [res.evaluation.energy, res.final_mse_rel, res.final_grad_rel, res.total_pcg_iters,
                float(jd.min()), float(jd.max()), time.perf_counter() - t0,
                STATUS_CODES.get(res.status, 3), len(res.records)]
@@ -77,7 +86,7 @@ def register_pair_fn(domain, problem, solver_cfg, objective: str = "deformation"
 
 def register_batch(pairs: Sequence | Callable, n_pairs: int | None = None, register_fn=None,
                    device=None, domain=None, problem=None, solver_cfg=None,
-                   objective: str = "deformation", group=None) -> BatchResult:
+                   objective: str = "deformation", group=None, in_flight: int = 1) -> BatchResult:
     """Register ``n_pairs`` (source, target) pairs sharded over the process group.
 
     ``pairs`` is a sequence of (source, target) or a callable ``i -> (source,
@@ -94,13 +103,36 @@ def register_batch(pairs: Sequence | Callable, n_pairs: int | None = None, regis
     mine = shard(n_pairs, rank, world)
     per_rank = -(-n_pairs // world)
     table = np.full((per_rank, len(STATS) + 1), np.nan)  # last column: pair index
-    atlas_sum = None
-    for slot, i in enumerate(mine):
-        src, tgt = get(i)
-        row, warped = register_fn(src, tgt)
+    warped_by_slot = {}
+    local = threading.local()
+
+    def work(slot, i):
+        if in_flight > 1 and torch.cuda.is_available():
+            if not hasattr(local, "stream"):
+                local.stream = torch.cuda.Stream()
+            with torch.cuda.stream(local.stream):
+                src, tgt = get(i)
+                row, warped = register_fn(src, tgt)
+                warped = warped.detach().to(torch.float64).clone()
+                local.stream.synchronize()
+        else:
+            src, tgt = get(i)
+            row, warped = register_fn(src, tgt)
+            warped = warped.detach().to(torch.float64)
+        return slot, i, row, warped
+
+    if in_flight > 1:
+        with ThreadPoolExecutor(max_workers=in_flight) as ex:
+            done = list(ex.map(lambda si: work(*si), list(enumerate(mine))))
+    else:
+        done = [work(slot, i) for slot, i in enumerate(mine)]
+    for slot, i, row, warped in done:
         table[slot, :len(STATS)] = row
         table[slot, -1] = i
-        w = warped.detach().to(torch.float64)
+        warped_by_slot[slot] = warped
+    atlas_sum = None
+    for slot in sorted(warped_by_slot):  # pair order: independent of in_flight
+        w = warped_by_slot[slot]
         atlas_sum = w.clone() if atlas_sum is None else atlas_sum + w
     if device is None:
         device = atlas_sum.device if atlas_sum is not None else torch.device("cpu")

@@ -101,3 +101,21 @@ def test_nan_velocity_fails_cfl():
     # reference transport.py:184: int(np.ceil(nan)) raises, as here
     with pytest.raises(ValueError):
         transport.check_cfl(flow)
+
+
+def test_batch_in_flight_pairs_match_serial():
+    """Several registrations in flight on one GPU (threads + streams) give the
+    same per-pair results and atlas as one at a time (bit-identical: every
+    (thread, stream) owns its context, and the atlas is summed in pair order)."""
+    import bench
+    from paper_1807_05117_b200 import batch as Bt
+
+    dom = B.Domain((32,) * 3, (8,) * 3, alpha=0.01)
+    pairs = [bench.blob_pair(dom, seed=s) for s in range(1, 6)]
+    prob = B.ProblemConfig(sigma2=0.03, n_time_steps=6)
+    cfg = B.SolverConfig(max_outer=6)
+    r1 = Bt.register_batch(pairs, domain=dom, problem=prob, solver_cfg=cfg, in_flight=1)
+    r3 = Bt.register_batch(pairs, domain=dom, problem=prob, solver_cfg=cfg, in_flight=3)
+    keep = [i for i, n in enumerate(Bt.STATS) if n != "wall_s"]
+    assert np.array_equal(r1.stats[:, keep], r3.stats[:, keep])
+    assert torch.equal(r1.atlas, r3.atlas)

@@ -124,7 +124,7 @@ def test_cli_register_end_to_end_deterministic(tmp_path):
     r = subprocess.run(cli + ["synthesize", "translation", "--size", "32", "--ndim", "2", "--shift", "0.08",
                               "--out", str(tmp_path)], capture_output=True, text=True, cwd=ROOT)
     assert r.returncode == 0, r.stderr
-    (tmp_path / "run.ini").write_text(CFG)
+    (tmp_path / "run.ini").write_text(CFG.replace("auto_refine = off", "auto_refine = on"))
     outs = []
     for _ in range(2):
         r = subprocess.run(cli + ["register", str(tmp_path / "run.ini")], capture_output=True, text=True, cwd=ROOT)
@@ -137,6 +137,10 @@ def test_cli_register_end_to_end_deterministic(tmp_path):
     assert "problem.objective = deformation" in text and "optimizer.max_outer = 12" in text
     rep = R.RegistrationReport.from_json((tmp_path / "out" / "report.json").read_text())
     assert rep.final_mse_rel < 100.0 and rep.jacobian_min > 0
+    # auto_refine off and a step count the CFL condition rejects: category exit code 4
+    (tmp_path / "cfl.ini").write_text(CFG.replace("max_outer = 12", "max_outer = 12\n"))
+    r = subprocess.run(cli + ["register", str(tmp_path / "cfl.ini")], capture_output=True, text=True, cwd=ROOT)
+    assert r.returncode == 4 and "CFL" in r.stderr
 
 
 @pytest.mark.gpu
