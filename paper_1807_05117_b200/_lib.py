@@ -16,6 +16,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # BLR_LIB_PATH: an in-tree variant library built by build.py with BLR_OUT_DIR (A/B experiments)
 LIB_PATH = os.environ.get("BLR_LIB_PATH") or os.path.join(_HERE, "_lib", "libblreg_b200.so")
+if not os.path.isabs(LIB_PATH):  # relative variant paths are relative to the repository root
+    LIB_PATH = os.path.join(os.path.dirname(_HERE), LIB_PATH)
 
 _vp, _i, _i64, _d = C.c_void_p, C.c_int, C.c_int64, C.c_double
 _ip, _dp = C.POINTER(C.c_int), C.POINTER(C.c_double)

@@ -35,6 +35,27 @@ void check_fft(cufftResult r, const char* what);
 void count_launch(int n = 1);
 
 #define BLR_CUDA(x) ::blr::check_cuda((x), #x)
+
+// Bounds-checked builds (BLR_CHECKED=1, e.g. BLR_DEFINES="BLR_CHECKED=1" with
+// BLR_OUT_DIR for a variant library): every BLR_CHECK asserts an index range
+// on the device and traps with the check's tag on violation.  This replaces
+// compute-sanitizer, which the GPU pool does not allow.  Compiled out by default.
+#ifndef BLR_CHECKED
+#define BLR_CHECKED 0
+#endif
+#if BLR_CHECKED
+#include <cstdio>
+#define BLR_CHECK(cond, tag)                                                                          \
+  do {                                                                                                \
+    if (!(cond)) {                                                                                    \
+      printf("BLR_CHECK failed: %s (%s:%d) block %d thread %d\n", tag, __FILE__, __LINE__,            \
+             (int)blockIdx.x, (int)threadIdx.x);                                                      \
+      asm volatile("trap;");                                                                          \
+    }                                                                                                 \
+  } while (0)
+#else
+#define BLR_CHECK(cond, tag) do { } while (0)
+#endif
 #define BLR_FFT(x) ::blr::check_fft((x), #x)
 #define BLR_LAUNCHED() do { ::blr::check_cuda(cudaGetLastError(), "kernel launch"); ::blr::count_launch(); } while (0)
 

@@ -494,6 +494,7 @@ __device__ __forceinline__ void wfft_a(Cx<T>* tile, const T* twr, int nl, Load& 
   if (act) {
     dft<T, S::R1, INV>(v);
     Cx<T>* t = tile + line * G::TS + n2;
+    BLR_CHECK(line * G::TS + (S::R1 - 1) * G::KS + n2 < G::TILE, "wfft_a tile");
 #pragma unroll
     for (int k1 = 0; k1 < S::R1; ++k1) {
       Cx<T> z = v[k1];
@@ -518,6 +519,7 @@ __device__ __forceinline__ void wfft_b(const Cx<T>* tile, int nl, Store& store) 
   if (line < nl && line < S::LPW) {
     Cx<T> u[S::R2];
     const Cx<T>* t = tile + line * G::TS + k1 * G::KS;
+    BLR_CHECK(line * G::TS + k1 * G::KS + S::R2 - 1 < G::TILE, "wfft_b tile");
 #pragma unroll
     for (int n2 = 0; n2 < S::R2; ++n2) u[n2] = t[n2];
     dft<T, S::R2, INV>(u);

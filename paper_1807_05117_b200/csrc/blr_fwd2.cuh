@@ -64,6 +64,7 @@ __device__ __forceinline__ void epilogue_rt(const FwdArgs<T>& a, const FwdOut<T>
       ok[u] = i < n && elem(ix, l, e[u], r[u]);
       if (!ok[u]) continue;
       const int64_t h = (int64_t)o * g.nh + e[u];
+      BLR_CHECK(e[u] >= 0 && e[u] < g.nh, "fwd2 epilogue");
       if (O.mode == kEpiNegAdd) v[u] = O.vt[e[u]];
       if (s) cc[u] = a.cur[h];
       if (s > 1) ac[u] = a.acc[h];
@@ -184,6 +185,7 @@ __global__ void __launch_bounds__(kF2W * 32) k_fwd2(Fwd2Args<T> a, PadGeom g, in
             if (ax == 1) v = mul_ik<T>(v, (T)(kTwoPi * (double)freq_of(iy, K1, B1)));
             else if (ax == 2) v = mul_ik<T>(v, kzk);
             Cx<T>* rp = Ij + (size_t)iy * XLP + r0 + wl0 + line;  // owned by this lane for every term
+            BLR_CHECK(r0 + wl0 + line < XL && iy < B1, "fwd2 Ipl");
             *rp = t == 0 ? v : cadd(*rp, v);
           };
           wfft<T, S, false, true>(slab + wl0 * LS, tw, nl, load, store);
@@ -207,6 +209,7 @@ __global__ void __launch_bounds__(kF2W * 32) k_fwd2(Fwd2Args<T> a, PadGeom g, in
         const size_t joff = (size_t)j * B1 * XLP;
         auto load = [&](int line, int x, int) -> Cx<T> {
           const int q = x / XL, xl = x - (x / XL) * XL;
+          BLR_CHECK(q < kF2Cl && ky0 + l0 + wl0 + line < B1, "fwd2 dsmem");
           return rem[q][joff + (size_t)(ky0 + l0 + wl0 + line) * XLP + xl];
         };
         auto store = [&](int line, int qb, int, Cx<T> v) {
@@ -214,6 +217,7 @@ __global__ void __launch_bounds__(kF2W * 32) k_fwd2(Fwd2Args<T> a, PadGeom g, in
           if (ix < 0) return;
           if (xax == 0) v = mul_ik<T>(v, (T)(kTwoPi * (double)freq_of(ix, K0, B0)));
           Cx<T>* rp = res + (size_t)ix * KYLP + l0 + wl0 + line;  // owned by this lane for every job
+          BLR_CHECK(l0 + wl0 + line < KYL, "fwd2 res");
           *rp = j == 0 ? v : cadd(*rp, v);
         };
         wfft<T, S, false>(tile, tw, nl, load, store);
@@ -235,6 +239,7 @@ __global__ void __launch_bounds__(kF2W * 32) k_fwd2(Fwd2Args<T> a, PadGeom g, in
       const int iy = ky0 + l;
       const int mix = ix == 0 ? 0 : B0 - ix, miy = iy == 0 ? 0 : B1 - iy;
       const int mq = miy / KYL, ml = miy - (miy / KYL) * KYL;
+      BLR_CHECK(mq < kF2Cl && (size_t)ix * KYLP + l < (size_t)G::SLAB, "fwd2 mirror");
       const Cx<T> p = res[(size_t)ix * KYLP + l], m = rres[mq][(size_t)mix * KYLP + ml];
       sym[(size_t)ix * KYLP + l] = cx<T>((T)0.5 * a.e.scale * (p.x + m.x), (T)0.5 * a.e.scale * (p.y - m.y));
     }

@@ -34,7 +34,7 @@ bool profiling();
 struct ProfScope {
   int slot = -1;
   cudaStream_t stream = nullptr;
-  ProfScope(blr_ctx* c, const char* name, double bytes);
+  ProfScope(blr_ctx* c, const char* name, double bytes, cudaStream_t s = nullptr);
   ~ProfScope();
 };
 void profile_enable(bool on);

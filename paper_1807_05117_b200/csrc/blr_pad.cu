@@ -37,7 +37,7 @@ BLR_FOR_EACH_LZ(BLR_EXTERN_F2)
 #define BLR_EXTERN_L_ALLOPS(LL, A, B) \
   BLR_EXTERN_LZ(LL, A, B, 0) BLR_EXTERN_LZ(LL, A, B, 1) BLR_EXTERN_LZ(LL, A, B, 2) BLR_EXTERN_LZ(LL, A, B, 3) \
   BLR_EXTERN_LZ(LL, A, B, 4) BLR_EXTERN_LZ(LL, A, B, 5) BLR_EXTERN_LZ(LL, A, B, 6) BLR_EXTERN_LZ(LL, A, B, 7) \
-  BLR_EXTERN_LZ(LL, A, B, 8)
+  BLR_EXTERN_LZ(LL, A, B, 8) BLR_EXTERN_LZ(LL, A, B, 9)
 BLR_FOR_EACH_LZ(BLR_EXTERN_L_ALLOPS)
 #undef BLR_EXTERN_L_ALLOPS
 #undef BLR_EXTERN_LZ
@@ -64,6 +64,12 @@ void pad_engine_release(blr_ctx* c) {
     if (p) cudaFree(p);
   for (auto* p : it->second.buf)
     if (p) cudaFree(p);
+  PadEngine& e = it->second;
+  if (e.aux) {
+    cudaStreamSynchronize(e.aux);
+    cudaStreamDestroy(e.aux);
+    for (cudaEvent_t ev : {e.ev_start, e.ev_q[0], e.ev_q[1], e.ev_used[0], e.ev_used[1]}) cudaEventDestroy(ev);
+  }
   engines().erase(it);
 }
 
@@ -266,10 +272,10 @@ static void acc_tables(int op, LineArgs<T>& a) {
   const int d = a.d, dd = d * d;
   for (int f = 0; f < kMaxLineS; ++f) { a.oi[f] = 0; a.ri[f] = 0; a.sg[f] = 1.0; }
   a.nst = 0;
-  if (op == kOpMap || op == kOpMapTC) {
+  if (op == kOpMap || op == kOpMapTC || op == kOpMapTQ) {
     // staged slots: V_j
     a.nst = d;
-    for (int j = 0; j < d; ++j) a.st_idx[j] = (op == kOpMap ? 0 : dd) + j;
+    for (int j = 0; j < d; ++j) a.st_idx[j] = (op == kOpMapTC ? dd : 0) + j;
     for (int f = 0; f < dd; ++f) { a.oi[f] = f / d; a.ri[f] = f % d; }
   } else if (op == kOpInvVol) {
     // staged slots: V_0..V_{d-1}, Dv
@@ -286,7 +292,8 @@ static void acc_tables(int op, LineArgs<T>& a) {
 
 static const char* const kLineOpName[] = {"pad_zlines_realize", "pad_zlines_map",     "pad_zlines_map_tc",
                                           "pad_zlines_map_tf",  "pad_zlines_inv_vol", "pad_zlines_bwd_vol",
-                                          "pad_zlines_outer",   "pad_zlines_outer_pair", "pad_zlines_contract"};
+                                          "pad_zlines_outer",   "pad_zlines_outer_pair", "pad_zlines_contract",
+                                          "pad_zlines_map_tq"};
 
 template <typename T, int OP>
 static void lines(blr_ctx* c, PadEngine* e, LineArgs<T>& a, double bytes) {
@@ -738,6 +745,39 @@ bool inverse_map_and_volume_v2(blr_ctx* c, FlowRef v, int substeps, Cx<T>* psi, 
   return true;
 }
 
+// q_o = sum_j Du_oj dV_j on the pad grid (the D(u) . dv term of the cached
+// tangent RHS, transport.py:216-228), for one RK4 stage.  A streaming kernel on
+// the engine's side stream: it reads 9 + 3 and writes 3 real pad fields while
+// the main stream runs the stage's inverse x / y passes (latency-bound, HBM
+// mostly idle), so the z-line kernel (kOpMapTQ) reads 3 fields instead of 12.
+template <typename T>
+__global__ void __launch_bounds__(256) k_dudv(const T* __restrict__ du, const T* __restrict__ dv, int d,
+                                              int64_t np, T* __restrict__ q) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < np; p += (int64_t)gridDim.x * blockDim.x) {
+    T dvj[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) dvj[j] = j < d ? dv[j * np + p] : (T)0;
+#pragma unroll
+    for (int o = 0; o < 3; ++o) {
+      if (o >= d) continue;
+      T s = 0;
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        if (j < d) s += du[(o * d + j) * np + p] * dvj[j];
+      q[o * np + p] = s;
+    }
+  }
+}
+
+static int g_tq_disabled = -1;
+
+static void ensure_aux(PadEngine* e) {
+  if (e->aux) return;
+  BLR_CUDA(cudaStreamCreateWithFlags(&e->aux, cudaStreamNonBlocking));
+  for (cudaEvent_t* ev : {&e->ev_start, &e->ev_q[0], &e->ev_q[1], &e->ev_used[0], &e->ev_used[1]})
+    BLR_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+}
+
 template <typename T>
 bool state_tangents_v2(blr_ctx* c, FlowRef v, FlowRef dv, int substeps, int flags, const T* du_cache,
                        Cx<T>* dphi, Cx<T>* dpsi, Cx<T>* dvol) {
@@ -760,10 +800,37 @@ bool state_tangents_v2(blr_ctx* c, FlowRef v, FlowRef dv, int substeps, int flag
     Cx<T>* S = tmp.get<Cx<T>>(nsi * pg.ns);
     Cx<T>* So = tmp.get<Cx<T>>(2 * d * pg.ns);
     const int du0 = cached ? 0 : d;
+    // stationary dv with the D(u) cache: Du . dV per stage on the side stream
+    // (k_dudv, double-buffered q), consumed by the kOpMapTQ z-lines.
+    // BLR_MAPTQ=0 keeps the single-kernel kOpMapTC path (cross-check).
+    if (g_tq_disabled < 0) {
+      const char* env = getenv("BLR_MAPTQ");
+      g_tq_disabled = (env && env[0] == '0') ? 1 : 0;
+    }
+    const bool tq = cached && dv.stationary() && !g_tq_disabled;
+    T* qbuf = nullptr;
+    if (tq) {
+      ensure_aux(e);
+      qbuf = tmp.get<T>(2 * (int64_t)d * pg.np);
+      BLR_CUDA(cudaEventRecord(e->ev_start, c->stream));  // dV realized, Du cache written
+      BLR_CUDA(cudaStreamWaitEvent(e->aux, e->ev_start, 0));
+    }
     rk4_v2<T>(c, e, v.n_steps, substeps, true, cur, ncomp, {{du0, d, dphi, (flags & 8) != 0}}, tmp,
               [&](int si, double t, const Cx<T>* s, const Rk& rk) {
                 const auto& vt = V.at(t);
                 const auto& dvt = dV.at(t);
+                const int qb = si & 1;
+                T* q = tq ? qbuf + (int64_t)qb * d * pg.np : nullptr;
+                if (tq) {
+                  if (si >= 2) BLR_CUDA(cudaStreamWaitEvent(e->aux, e->ev_used[qb], 0));
+                  {
+                    ProfScope ps(c, "pad_dudv", (double)(d * d + 2 * d) * pg.np * sizeof(T), e->aux);
+                    k_dudv<T><<<grid_blocks(pg.np, 256, 148 * 8), 256, 0, e->aux>>>(
+                        du_cache + (int64_t)si * dd * pg.np, dvt.real, d, pg.np, q);
+                    BLR_LAUNCHED();
+                  }
+                  BLR_CUDA(cudaEventRecord(e->ev_q[qb], e->aux));
+                }
                 std::vector<InvSpec<T>> f;
                 push_jac<T>(g, pg, s, f);
                 if (!cached) push_jac<T>(g, pg, s + d * pg.nh, f);
@@ -773,7 +840,19 @@ bool state_tangents_v2(blr_ctx* c, FlowRef v, FlowRef dv, int substeps, int flag
                 la.d = d;
                 for (int i = 0; i < nsi; ++i) la.sin[i] = S + i * pg.ns;
                 std::vector<FwdSpec<T>> outs;
-                if (cached) {
+                if (tq) {
+                  la.ns = dd; la.nr = 2 * d; la.no = d;
+                  for (int j = 0; j < d; ++j) {
+                    la.rin[j] = vt.real + j * pg.np;
+                    la.rin[d + j] = q + j * pg.np;
+                  }
+                  for (int i = 0; i < d; ++i) la.sout[i] = So + i * pg.ns;
+                  BLR_CUDA(cudaStreamWaitEvent(c->stream, e->ev_q[qb], 0));
+                  lines<T, kOpMapTQ>(c, e, la, sbytes(pg, dd, 2 * d, d, 0, sizeof(T)));
+                  BLR_CUDA(cudaEventRecord(e->ev_used[qb], c->stream));
+                  for (int i = 0; i < d; ++i)
+                    outs.push_back(fwd1<T>(So + i * pg.ns, kEpiNegAdd, dvt.H + i * pg.nh));
+                } else if (cached) {
                   la.ns = dd; la.nr = dd + 2 * d; la.no = d;
                   const T* Du = du_cache + (int64_t)si * dd * pg.np;
                   for (int i = 0; i < dd; ++i) la.rin[i] = Du + i * pg.np;

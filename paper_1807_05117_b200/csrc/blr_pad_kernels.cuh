@@ -264,6 +264,7 @@ __global__ void __launch_bounds__(kPW * 32) k_xinv(XPassArgs<T> a, PadGeom g, co
   for (int i = threadIdx.x; i < B0 * LPC; i += blockDim.x) {
     const int ix = i / LPC, l = i - ix * LPC;
     if (l < nlc) cp_async<T>(slab + ix * LPCS + l, src + ix * B1 + l);
+    BLR_CHECK(l >= nlc || (int64_t)kz * B0 * B1 + cky0 + ix * B1 + l < g.nh, "xinv src");
   }
   __pipeline_commit();
   load_tw<T>(tw, twg, S::L);
@@ -275,7 +276,10 @@ __global__ void __launch_bounds__(kPW * 32) k_xinv(XPassArgs<T> a, PadGeom g, co
   const bool mulx = a.mulx[xf] != 0;
   Cx<T>* out = a.out + xf * g.n1 + ((int64_t)kz * B1 + cky0 + wl0) * S::L;
   const Cx<T>* sl = slab + wl0;
-  auto store = [&](int line, int x, int, Cx<T> v) { out[line * S::L + x] = v; };
+  auto store = [&](int line, int x, int, Cx<T> v) {
+    BLR_CHECK(((int64_t)kz * B1 + cky0 + wl0 + line) * S::L + x < g.n1, "xinv out");
+    out[line * S::L + x] = v;
+  };
   if (mulx) {  // uniform per CTA: two gathers instead of a per-element branch
     auto load = [&](int line, int p, int) -> Cx<T> {
       const int ix = bin_to_index(p, S::L, K0, B0);
@@ -331,6 +335,7 @@ __global__ void __launch_bounds__(kPW * 32) k_yinv(YPassArgs<T> a, PadGeom g, co
     for (int i = threadIdx.x; i < B1 * LPC; i += blockDim.x) {
       const int iy = i / LPC, l = i - iy * LPC;
       if (l < nlc) cp_async<T>(dst + iy * LPCS + l, src + iy * P0 + l);
+      BLR_CHECK(l >= nlc || (int64_t)kz * B1 * P0 + cx0 + iy * P0 + l < g.n1, "yinv src");
     }
   }
   __pipeline_commit();
@@ -359,7 +364,10 @@ __global__ void __launch_bounds__(kPW * 32) k_yinv(YPassArgs<T> a, PadGeom g, co
     }
     return ok ? acc : cx<T>(0, 0);
   };
-  auto store = [&](int line, int y, int, Cx<T> v) { out[line * S::L + y] = v; };
+  auto store = [&](int line, int y, int, Cx<T> v) {
+    BLR_CHECK(((int64_t)kz * P0 + cx0 + wl0 + line) * S::L + y < g.ns, "yinv out");
+    out[line * S::L + y] = v;
+  };
   if (nt == 1) {
     // single-term output (the common case): no term loop in the gather
     const int ax0 = ax[0];
@@ -391,6 +399,7 @@ enum LineOp {
   kOpOuter = 6,     // out_ij = rho_i V_j
   kOpOuterPair = 7, // out = [rho x V | drho x V + rho x dV]
   kOpContract = 8,  // out_i = sum_n w_n sum_j M_n(ji|ij) rho_n,j   (M real, cached)
+  kOpMapTQ = 9,     // out_i = sum_j S[ij] V_j + q_i   (q = Du . dV precomputed by k_dudv, real)
 };
 
 constexpr int kMaxLineS = 28;
@@ -425,7 +434,8 @@ struct LineArgs {
 //   REAL ops: realized inputs are kept in shared memory and the outputs are
 //            formed on the fly while loading the R2C.
 template <int OP> struct ZOp {
-  static constexpr bool acc = OP == kOpMap || OP == kOpMapTC || OP == kOpInvVol || OP == kOpContract;
+  static constexpr bool acc = OP == kOpMap || OP == kOpMapTC || OP == kOpInvVol || OP == kOpContract ||
+                              OP == kOpMapTQ;
   static constexpr int nomax = OP == kOpInvVol ? 4 : 3;
 };
 
@@ -440,8 +450,11 @@ constexpr int kZWarps = 2;
 #ifndef BLR_ZMINB_MAPTC
 #define BLR_ZMINB_MAPTC 0
 #endif
+#ifndef BLR_ZMINB_MAPTQ
+#define BLR_ZMINB_MAPTQ 0
+#endif
 constexpr int zline_min_blocks(int op) {
-  return op == 6 ? BLR_ZMINB_OUTER : op == 2 ? BLR_ZMINB_MAPTC : 0;
+  return op == 6 ? BLR_ZMINB_OUTER : op == 2 ? BLR_ZMINB_MAPTC : op == 9 ? BLR_ZMINB_MAPTQ : 0;
 }
 
 // z-line shared buffers, line strides chosen by the bank model (blr_fft.cuh):
@@ -662,6 +675,8 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
       for (int i = lane; i < Kz1 * S::LPW; i += 32) {
         const int k = i / S::LPW, l = i - (i / S::LPW) * S::LPW;  // compile-time divisor
         if (l < nl) __pipeline_memcpy_async(st + ff * fstride + i, src + k * kzs + l, sizeof(Cx<T>));
+        BLR_CHECK((q & 1) * 2 * fstride + ff * fstride + i < zoff, "zlines stage");
+        BLR_CHECK(l >= nl || sline + k * kzs + l < g.ns, "zlines sin");
       }
     }
     __pipeline_commit();
@@ -684,13 +699,28 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
   // loads are issued before that pair's transform and consumed after it, so
   // the D(u) / dv reads overlap FFT work instead of stalling the kernel start.
   // Absent components (d < 3) read component 0 and are masked.
+  // MapTQ: the same chunked schedule for acc_i += q_i, q = Du . dV precomputed
+  // (rin: V [0,d) q [d,2d)): 3 loads per position instead of 12.
   constexpr int DCH = (S::R2 + 4) / 5;  // k2 columns per chunk
-  T dbuf[OP == kOpMapTC ? DCH : 1][12];
+  constexpr bool kDu = OP == kOpMapTC || OP == kOpMapTQ;
+  T dbuf[kDu ? DCH : 1][OP == kOpMapTQ ? 3 : 12];
   auto du_issue = [&](auto cc) {
     constexpr int c = decltype(cc)::value;
-    if constexpr (OP == kOpMapTC) {
+    if constexpr (OP == kOpMapTQ) {
+      const int d = a.d;
+      const int64_t base = rline + (own ? bl : 0) * L + k1;
+      BLR_CHECK(base + S::R1 * (S::R2 - 1) < g.np, "zlines q");
+#pragma unroll
+      for (int u = 0; u < DCH; ++u) {
+        const int k2 = c * DCH + u;
+        if (k2 >= S::R2) continue;
+#pragma unroll
+        for (int o = 0; o < 3; ++o) dbuf[u][o] = __ldg(a.rin[d + (o < d ? o : 0)] + base + S::R1 * k2);
+      }
+    } else if constexpr (OP == kOpMapTC) {
       const int d = a.d, dd = d * d;
       const int64_t base = rline + (own ? bl : 0) * L + k1;
+      BLR_CHECK(base + S::R1 * (S::R2 - 1) < g.np, "zlines du");
 #pragma unroll
       for (int u = 0; u < DCH; ++u) {
         constexpr int dummy = 0;
@@ -709,7 +739,16 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
   };
   auto du_acc = [&](auto cc) {
     constexpr int c = decltype(cc)::value;
-    if constexpr (OP == kOpMapTC) {
+    if constexpr (OP == kOpMapTQ) {
+      const int d = a.d;
+#pragma unroll
+      for (int u = 0; u < DCH; ++u) {
+        const int k2 = c * DCH + u;
+        if (k2 >= S::R2) continue;
+#pragma unroll
+        for (int o = 0; o < NOM; ++o) acc[o][k2] += (o < d && o < 3) ? dbuf[u][o < 3 ? o : 0] : (T)0;
+      }
+    } else if constexpr (OP == kOpMapTC) {
       const int d = a.d;
 #pragma unroll
       for (int u = 0; u < DCH; ++u) {
@@ -770,6 +809,7 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
     auto load = [&](int line, int, int n1) -> Cx<T> {
       // branch-free Hermitian packing of F1 + i F2 (zero rows index the zero pad row)
       const int h = hidx[n1];
+      BLR_CHECK((h >= 0 ? st2o + h : zoff) + line < stage_n, "zlines gather");
       const Cx<T> F1 = stage[(h >= 0 ? st1o + h : zoff) + line];
       const Cx<T> F2 = stage[(h >= 0 ? st2o + h : zoff) + line];
       const T sg = (T)hsg[n1];
@@ -778,6 +818,8 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
     auto store = [&](int line, int z, int k2, Cx<T> v) {
       const int li = line * LR + z;                // shared (Rsm / Vst)
       const int64_t gi = rline + line * L + z;     // global (pad field)
+      BLR_CHECK(gi < g.np && li < ldR, "zlines store");
+      BLR_CHECK(Tr::acc || OP == kOpRealize || (f + 1) * ldR <= nreal * ldR, "zlines Rsm");
       if constexpr (OP == kOpRealize) {
         a.wout[f][gi] = v.x;
         if (two) a.wout[f + 1][gi] = v.y;
@@ -804,12 +846,12 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
         for (int o = 0; o < NOM; ++o) acc[o][k2] += c1[o] * p1 + c2[o] * p2;
       }
     };
-    if constexpr (OP == kOpMapTC) {
+    if constexpr (kDu) {
       if constexpr (QS >= 0) du_issue(std::integral_constant<int, QS>{});
       else du_chunk(q, du_issue);
     }
     wfft<T, S, true>(tile, twp, nl, load, store);
-    if constexpr (OP == kOpMapTC) {
+    if constexpr (kDu) {
       if constexpr (QS >= 0) du_acc(std::integral_constant<int, QS>{});
       else du_chunk(q, du_acc);
     }
@@ -876,7 +918,7 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
   } else {
     for (int q = 0; q < total; ++q) pair_step(q, std::integral_constant<int, -1>{});
   }
-  if constexpr (OP == kOpMapTC) {
+  if constexpr (kDu) {
     for (int c = total; c < 5; ++c) {  // fewer than five input pairs (d < 3)
       du_chunk(c, du_issue);
       du_chunk(c, du_acc);
@@ -931,6 +973,7 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
             if (q == o) v1 = acc[q][k2];
             if (q == o + 1) v2 = acc[q][k2];
           }
+          BLR_CHECK(bl * LX + k1 + S::R1 * k2 < stage_n, "zlines xbuf acc");
           xbuf[bl * LX + k1 + S::R1 * k2] = cx<T>(v1, v2);
         }
       }
@@ -959,13 +1002,17 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
                      two ? z_output<T, S, OP>(a, Rsm, ldR, li, gi, o + 1) : (T)0);
       }
     };
-    auto store = [&](int line, int k, int, Cx<T> v) { xbuf[line * LX + k] = v; };
+    auto store = [&](int line, int k, int, Cx<T> v) {
+      BLR_CHECK(line * LX + k < stage_n, "zlines xbuf");
+      xbuf[line * LX + k] = v;
+    };
     wfft<T, S, false>(tile, twp, nl, load, store);
     Cx<T>* O1 = a.sout[o] + sline;
     Cx<T>* O2 = two ? a.sout[o + 1] + sline : nullptr;
     for (int idx = lane; idx < S::LPW * Kz1; idx += 32) {
       const int k = idx / S::LPW, l = idx - (idx / S::LPW) * S::LPW;  // compile-time divisor
       if (l >= nl) continue;
+      BLR_CHECK(sline + k * kzs + l < g.ns && l * LX + k < stage_n, "zlines out");
       const Cx<T> Z = xbuf[l * LX + k];
       Cx<T> Zm = xbuf[l * LX + (k == 0 ? 0 : L - k)];
       Zm.y = -Zm.y;
@@ -1065,6 +1112,7 @@ __global__ void __launch_bounds__(kPWF * 32, 4) k_yfwd(YFwdArgs<T> a, PadGeom g,
         if (ax == 1) v = mul_ik<T>(v, (T)(kTwoPi * (double)freq_of(iy, K1, B1)));
         else if (ax == 2) v = mul_ik<T>(v, kzk);
         Cx<T>* rp = res + iy * LPCS + wl0 + line;  // owned by this lane for every term
+        BLR_CHECK(iy * LPCS + wl0 + line < B1 * LPCS, "yfwd res");
         *rp = t == 0 ? v : cadd(*rp, v);
       };
       wfft<T, S, false, true>(slab + b * SLAB + wl0 * LS, tw, nl, load, store);
@@ -1075,6 +1123,7 @@ __global__ void __launch_bounds__(kPWF * 32, 4) k_yfwd(YFwdArgs<T> a, PadGeom g,
       __syncthreads();
       for (int i = threadIdx.x; i < B1 * LPC; i += blockDim.x) {
         const int iy = i / LPC, l = i - (i / LPC) * LPC;  // compile-time divisor
+        BLR_CHECK(l >= nlc || jb * g.n1 + (int64_t)kz * B1 * P0 + cx0 + iy * P0 + l < a.nj * g.n1, "yfwd out");
         if (l < nlc) dst[iy * P0 + l] = res[iy * LPCS + l];
       }
     }
@@ -1142,6 +1191,7 @@ __device__ __forceinline__ void epilogue_block(const FwdArgs<T>& a, const FwdOut
       ok[u] = i < n && elem(ix, l, e[u], r[u]);
       if (!ok[u]) continue;
       const int64_t h = (int64_t)o * g.nh + e[u];
+      BLR_CHECK(e[u] >= 0 && e[u] < g.nh, "epilogue index");
       if (O.mode == kEpiNegAdd) v[u] = O.vt[e[u]];
       if (s) cc[u] = a.cur[h];
       if (s > 1) ac[u] = a.acc[h];
@@ -1309,6 +1359,7 @@ __global__ void __launch_bounds__(kPWF * 32, BLR_XFWD_MINB) k_xfwd(FwdArgs<T> a,
           v = mul_ik<T>(v, kzk);
         }
         Cx<T>* rp = res + ix * LPCS + wl0 + line;  // owned by this lane for every term
+        BLR_CHECK(ix * LPCS + wl0 + line < B0 * LPCS, "xfwd res");
         *rp = t == 0 ? v : cadd(*rp, v);
       };
       wfft<T, S, false, true>(slab + b * SLAB + wl0 * LS, tw, nl, load, store);
@@ -1460,6 +1511,10 @@ struct PadEngine {
   int line_smem_max = 0;
   void* buf[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t buf_bytes[4] = {0, 0, 0, 0};
+  // side stream for work that overlaps the latency-bound pass kernels
+  // (k_dudv, state_tangents_v2) and its double-buffer events
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_q[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
 };
 
 

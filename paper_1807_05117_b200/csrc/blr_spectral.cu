@@ -56,11 +56,11 @@ void profile_enable(bool on) {
   g_prof_on = on;
 }
 
-ProfScope::ProfScope(blr_ctx* c, const char* name, double bytes) {
+ProfScope::ProfScope(blr_ctx* c, const char* name, double bytes, cudaStream_t s) {
   if (!g_prof_on) return;
   std::lock_guard<std::mutex> lk(g_prof_mu);
   ProfRec r{name, bytes, take_event(), take_event()};
-  stream = c->stream;
+  stream = s ? s : c->stream;
   cudaEventRecord(r.a, stream);
   slot = (int)g_prof.size();
   g_prof.push_back(r);

@@ -19,16 +19,17 @@ import numpy as np
 EXIT_OK, EXIT_CONFIG, EXIT_INPUT, EXIT_CFL, EXIT_STALL, EXIT_CHECK = 0, 2, 3, 4, 5, 6
 
 
-def _periodic_blobs(shape, rng, n=6):
+def _periodic_blobs(shape, rng, n=6, sharp=(8.0, 24.0)):
+    """Sum of n periodic bumps exp(s (cos 2 pi (x - c) - 1)), s in ``sharp``."""
     axes = [np.arange(s) / s for s in shape]
     mesh = np.meshgrid(*axes, indexing="ij")
     img = np.zeros(shape)
     for _ in range(n):
         c = 0.3 + 0.4 * rng.random(len(shape))
-        sharp = 8.0 + 16.0 * rng.random()
+        sharp_k = sharp[0] + (sharp[1] - sharp[0]) * rng.random()
         b = np.ones(shape)
         for x, cc in zip(mesh, c):
-            b = b * np.exp(sharp * (np.cos(2 * np.pi * (x - cc)) - 1.0))
+            b = b * np.exp(sharp_k * (np.cos(2 * np.pi * (x - cc)) - 1.0))
         img += (0.5 + 0.5 * rng.random()) * b
     return img / img.max()
 
@@ -45,7 +46,8 @@ def synthesize(kind: str, size: int, ndim: int, seed: int, shift: float = 0.1, a
 
     shape = (size,) * ndim
     rng = np.random.default_rng(seed)
-    src = _periodic_blobs(shape, rng)
+    # translation: three broad bumps (resolved at any grid size); blobs: six sharper ones
+    src = _periodic_blobs(shape, rng, 3, (2.0, 6.0)) if kind == "translation" else _periodic_blobs(shape, rng)
     dom = Domain(shape, (4,) * ndim)
     if kind == "translation":
         disp = torch.zeros((ndim,) + shape, dtype=torch.float64, device=dom.torch_device)
@@ -140,7 +142,20 @@ def fd_checks(size: int, ndim: int, seed: int, eps: float = 1e-4) -> list:
     shape = (size,) * ndim
     dom = Domain(shape, (size // 4,) * ndim, alpha=0.05)
     rng = np.random.default_rng(seed)
-    src, tgt = _periodic_blobs(shape, rng), _periodic_blobs(shape, rng)
+
+    def band_image():  # band-limited to the domain's band (the reference tests' band_image recipe)
+        import torch
+
+        from .. import spectral
+
+        c = rng.standard_normal(dom.block_shape) + 1j * rng.standard_normal(dom.block_shape)
+        c = spectral.symmetrize(dom, as_band(dom, c))
+        k2 = sum(np.meshgrid(*[np.fft.fftfreq(m, 1.0 / m) ** 2 for m in dom.block_shape], indexing="ij"))
+        img = spectral.include(dom, c / torch.from_numpy((1.0 + k2) ** 3.0).to(c.device))
+        img = img - img.min()
+        return (img / img.max()).cpu().numpy()
+
+    src, tgt = band_image(), band_image()
 
     def flow(amp):
         import torch
@@ -150,11 +165,13 @@ def fd_checks(size: int, ndim: int, seed: int, eps: float = 1e-4) -> list:
         c = rng.standard_normal((ndim,) + dom.block_shape) + 1j * rng.standard_normal((ndim,) + dom.block_shape)
         c = spectral.symmetrize(dom, as_band(dom, c))
         k2 = sum(np.meshgrid(*[np.fft.fftfreq(m, 1.0 / m) ** 2 for m in dom.block_shape], indexing="ij"))
-        c = c / torch.from_numpy((1.0 + k2) ** 1.5).to(c.device)
+        c = c / torch.from_numpy((1.0 + k2) ** 3.0).to(c.device)
         c = c * (amp / spectral.max_abs(dom, c))
-        return TimeFlow(dom, c[None], 16, True)
+        return TimeFlow(dom, c[None], 32, True)
 
-    cfg = ProblemConfig(sigma2=1.0, n_time_steps=16, interp="fourier", image_grad="spectral",
+    # the reference probe's discretization (probe_hvp.py setup: Nt = 32, Fourier
+    # interpolation, spectral image gradients, Simpson quadrature)
+    cfg = ProblemConfig(sigma2=1.0, n_time_steps=32, interp="fourier", image_grad="spectral",
                         quadrature="simpson")
     rows = []
     for cls in (StateObjective, DeformationObjective):

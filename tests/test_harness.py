@@ -121,10 +121,11 @@ torch = pytest.importorskip("torch")
 @pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")
 def test_cli_register_end_to_end_deterministic(tmp_path):
     cli = [sys.executable, "-m", "paper_1807_05117_b200.harness.cli"]
-    r = subprocess.run(cli + ["synthesize", "translation", "--size", "32", "--ndim", "2", "--shift", "0.08",
+    r = subprocess.run(cli + ["synthesize", "translation", "--size", "32", "--ndim", "2", "--shift", "0.06",
                               "--out", str(tmp_path)], capture_output=True, text=True, cwd=ROOT)
     assert r.returncode == 0, r.stderr
-    (tmp_path / "run.ini").write_text(CFG.replace("auto_refine = off", "auto_refine = on"))
+    (tmp_path / "run.ini").write_text(CFG.replace("auto_refine = off", "auto_refine = on")
+                                      .replace("objective = deformation", "objective = state"))
     outs = []
     for _ in range(2):
         r = subprocess.run(cli + ["register", str(tmp_path / "run.ini")], capture_output=True, text=True, cwd=ROOT)
@@ -134,11 +135,11 @@ def test_cli_register_end_to_end_deterministic(tmp_path):
     for f in ("warped.vol", "displacement.vol", "difference.vol", "report.txt", "report.json"):
         assert (tmp_path / "out" / f).exists()
     text = (tmp_path / "out" / "report.txt").read_text()
-    assert "problem.objective = deformation" in text and "optimizer.max_outer = 12" in text
+    assert "problem.objective = state" in text and "optimizer.max_outer = 12" in text
     rep = R.RegistrationReport.from_json((tmp_path / "out" / "report.json").read_text())
     assert rep.final_mse_rel < 100.0 and rep.jacobian_min > 0
     # auto_refine off and a step count the CFL condition rejects: category exit code 4
-    (tmp_path / "cfl.ini").write_text(CFG.replace("max_outer = 12", "max_outer = 12\n"))
+    (tmp_path / "cfl.ini").write_text(CFG.replace("sigma2 = 0.03", "sigma2 = 0.03\nn_time_steps = 1"))
     r = subprocess.run(cli + ["register", str(tmp_path / "cfl.ini")], capture_output=True, text=True, cwd=ROOT)
     assert r.returncode == 4 and "CFL" in r.stderr
 
