@@ -438,19 +438,21 @@ constexpr int tile_cost(int TS, int KS, int E) {
     c += wavefronts([&](int l) { return l / S::R1 < S::LPW ? (l / S::R1) * TS + (l % S::R1) * KS + n2 : -1; }, E);
   return c;
 }
-// BLR_BANKPAD=1 selects the bank-model strides; the default keeps the dense
-// tile (KS = R2 + 1).  A/B on the B200 (r02): the conflict-free layout cut the
-// z-line kernels' shared wavefronts by 30-45% but not their time (they are
-// latency-bound at 8-12 warps per SM), and its larger footprint cost the
-// outer op a CTA per SM, so it is off.
+// Bank-model strides: always for fp32, for fp64 only with BLR_BANKPAD=1.  A/B
+// on the B200 (r02): in fp64 the conflict-free layout cut the z-line kernels'
+// shared wavefronts by 30-45% but not their time (latency-bound at 8-12 warps
+// per SM) and its larger footprint cost the outer op a CTA per SM (deformation
+// GN HVP 10.25 vs 10.0 ms); in fp32 it is a win (7.08 vs 7.56 ms).
 #ifndef BLR_BANKPAD
 #define BLR_BANKPAD 0
 #endif
+template <typename T>
+constexpr bool bank_pad() { return BLR_BANKPAD || sizeof(T) == 4; }
 template <typename T, class S>
 struct TileG {
   static constexpr int E = (int)(2 * sizeof(T));
   static constexpr int best() {  // KS * 256 + TS
-    if (!BLR_BANKPAD) return (S::R2 + 1) * 256 + S::R1 * (S::R2 + 1);
+    if (!bank_pad<T>()) return (S::R2 + 1) * 256 + S::R1 * (S::R2 + 1);
     int bc = 1 << 30, bv = 0;
     for (int ks = S::R2; ks < S::R2 + 8; ++ks) {
       const int base = (S::R1 - 1) * ks + S::R2;

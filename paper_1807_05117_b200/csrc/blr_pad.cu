@@ -800,12 +800,15 @@ bool state_tangents_v2(blr_ctx* c, FlowRef v, FlowRef dv, int substeps, int flag
     Cx<T>* S = tmp.get<Cx<T>>(nsi * pg.ns);
     Cx<T>* So = tmp.get<Cx<T>>(2 * d * pg.ns);
     const int du0 = cached ? 0 : d;
-    // stationary dv with the D(u) cache: Du . dV per stage on the side stream
-    // (k_dudv, double-buffered q), consumed by the kOpMapTQ z-lines.
-    // BLR_MAPTQ=0 keeps the single-kernel kOpMapTC path (cross-check).
+    // Opt-in (BLR_MAPTQ=1): with the D(u) cache and a stationary dv, compute
+    // Du . dV per stage on the side stream (k_dudv, double-buffered q) and let
+    // the kOpMapTQ z-lines read 3 real fields instead of 12.  A/B on the B200
+    // (r02): map_tq 2.54 vs map_tc 2.81 ms per HVP, but k_dudv (1.45 ms) does
+    // not overlap the pass kernels (their CTAs hold the SMs; xfwd slows down),
+    // deformation GN HVP 10.47 vs 9.78 ms -- so the single-kernel MapTC stays.
     if (g_tq_disabled < 0) {
       const char* env = getenv("BLR_MAPTQ");
-      g_tq_disabled = (env && env[0] == '0') ? 1 : 0;
+      g_tq_disabled = (env && env[0] == '1') ? 0 : 1;
     }
     const bool tq = cached && dv.stationary() && !g_tq_disabled;
     T* qbuf = nullptr;

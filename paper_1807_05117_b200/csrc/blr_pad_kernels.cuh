@@ -484,7 +484,7 @@ struct ZLineG {
     return c;
   }
   static constexpr int pick(bool real) {
-    if (!BLR_BANKPAD) return L;
+    if (!bank_pad<T>()) return L;
     int best = L, bc = 1 << 30;
     for (int p = 0; p < 8; ++p) {
       const int c = real ? rcost(L + p) : xcost(L + p);
