@@ -98,24 +98,26 @@ __device__ __forceinline__ void epilogue_rt(const FwdArgs<T>& a, const FwdOut<T>
 }
 
 // shared layout (complex entries unless noted):
-//   tw  [2L] T | slab [ROWS][LS] (phase-1 rows, warp tiles overlay their rows;
-//   phase 2: per-warp x-FFT tiles) | Ipl [nj][B1][XLP] | res [B0][KYLP]
+//   tw [2L] T | slab [2][ROWS][LS] (phase 1: double-buffered rows, warp tiles
+//   overlay their rows; phase 2: x-FFT tiles + res [B0][KYLP] overlay it) |
+//   I [KYL][XP]: this CTA's ky lines over every x, written by the whole cluster
 template <typename T, class S>
 struct Fwd2Geom {
-  static constexpr int ROWS = kF2W * S::LPW;             // rows per phase-1 round
+  static constexpr int ROWS = kF2W * S::LPW;             // rows per phase-1 step
   static constexpr int LS = row_stride<T, S, true>();    // slab row stride (>= tile stride)
   static constexpr int SLAB = ROWS * LS;
-  static_assert(SLAB >= kF2W * TileG<T, S>::TILE, "phase-2 tiles overlay the slab");
+  static_assert(SLAB >= kF2W * TileG<T, S>::TILE, "tiles overlay the slab");
   __host__ __device__ static int xl(int P) { return (P + kF2Cl - 1) / kF2Cl; }
-  __host__ __device__ static int xlp(int P) { return xl(P) | 1; }
+  __host__ __device__ static int xp(int P) { return P | 1; }
   __host__ __device__ static int kyl(int B1) { return (B1 + kF2Cl - 1) / kF2Cl; }
   __host__ __device__ static int kylp(int B1) { return kyl(B1) | 1; }
-  static size_t smem(const PadGeom& g, int nj) {
-    return sizeof(T) * 2 * S::L + sizeof(Cx<T>) * ((size_t)SLAB + (size_t)nj * g.B[1] * xlp(g.P[0]) +
-                                                    (size_t)g.B[0] * kylp(g.B[1]));
+  static size_t smem(const PadGeom& g, int) {
+    return sizeof(T) * 2 * S::L + sizeof(Cx<T>) * (2 * (size_t)SLAB + (size_t)kyl(g.B[1]) * xp(g.P[0]));
   }
 };
 
+// One launch per projection of single-job outputs (every output's x pass sums
+// one I field; the flux divergence's two-job outputs keep the two-kernel path).
 template <typename T, class S>
 __global__ void __launch_bounds__(kF2W * 32) k_fwd2(Fwd2Args<T> a, PadGeom g, int njmax,
                                                     const double* __restrict__ twg) {
@@ -127,11 +129,10 @@ __global__ void __launch_bounds__(kF2W * 32) k_fwd2(Fwd2Args<T> a, PadGeom g, in
   const int unit = blockIdx.x / kF2Cl;
   const int o = unit / g.Kz1, kz = unit - (unit / g.Kz1) * g.Kz1;
   const int P = g.P[0], B0 = g.B[0], B1 = g.B[1], K0 = g.K[0], K1 = g.K[1];
-  const int XL = G::xl(P), XLP = G::xlp(P), KYL = G::kyl(B1), KYLP = G::kylp(B1);
+  const int XL = G::xl(P), XP = G::xp(P), KYL = G::kyl(B1), KYLP = G::kylp(B1);
   T* tw = (T*)smem_raw;
-  Cx<T>* slab = (Cx<T>*)(tw + 2 * L);
-  Cx<T>* Ipl = slab + G::SLAB;           // [nj][B1][XLP]
-  Cx<T>* res = Ipl + (size_t)njmax * B1 * XLP;  // [B0][KYLP]
+  Cx<T>* slab = (Cx<T>*)(tw + 2 * L);  // [2][SLAB]
+  Cx<T>* Iown = slab + 2 * G::SLAB;    // [KYL][XP]
   const int warp = threadIdx.x >> 5;
   const int wl0 = warp * LPW;
   __shared__ uint64_t bars[2];
@@ -139,9 +140,8 @@ __global__ void __launch_bounds__(kF2W * 32) k_fwd2(Fwd2Args<T> a, PadGeom g, in
   stg.init(bars);
   load_tw<T>(tw, twg, L);
   const FwdOut<T>& O = a.e.o[o];
-  const int nj = a.nj[o];
+  const Fwd2Job<T>& J = a.job[o][0];
   const T kzk = (T)(kTwoPi * (double)kz);
-  // prefetch this CTA's epilogue operand rows (ky chunk, every kx) into L1
   const int ky0 = rank * KYL, nky = max(0, min(KYL, B1 - ky0));
   if (kXfwdPrefetch && nky > 0 && (a.e.rk_s || O.mode == kEpiNegAdd)) {
     for (int r = threadIdx.x; r < 2 * B0; r += blockDim.x) {
@@ -153,93 +153,95 @@ __global__ void __launch_bounds__(kF2W * 32) k_fwd2(Fwd2Args<T> a, PadGeom g, in
       if (a.e.rk_s > 1) prefetch_l1(a.e.acc + h);
     }
   }
+  Cx<T>* rem[kF2Cl];
+#pragma unroll
+  for (int q = 0; q < kF2Cl; ++q) rem[q] = cluster.map_shared_rank(Iown, q);
   __syncthreads();  // mbarrier init + twiddles
   pdl_wait();
 
-  // ---- phase 1: forward y FFTs of this CTA's x rows into its I slice ----
+  // ---- phase 1: forward y FFTs of this CTA's x rows, pushed to the owners ----
+  // steps (round r0, term t), double-buffered: step k+1's rows stream in while
+  // step k is transformed; each lane keeps its outputs of one round in
+  // registers across the terms and stores them once, to the CTA that owns the
+  // ky line (st.shared::cluster: no load latency on the critical path)
   const int x0 = rank * XL, nx = max(0, min(XL, P - x0));
-  for (int j = 0; j < nj; ++j) {
-    const Fwd2Job<T>& J = a.job[o][j];
-    Cx<T>* Ij = Ipl + (size_t)j * B1 * XLP;
-    for (int r0 = 0; r0 < nx; r0 += G::ROWS) {
-      const int nr = min(G::ROWS, nx - r0);
-      for (int t = 0; t < J.nt; ++t) {
-        const Cx<T>* src = J.s[t] + ((int64_t)kz * P + x0 + r0) * L;  // nr contiguous rows
-        stg.begin(0, (uint32_t)(nr * L * sizeof(Cx<T>)));
-        stg.rows(slab, LS, src, L, nr, L, 0);
-        stg.commit();
-        if constexpr (Stager<T>::kBulk) {
-          stg.wait(0);
-        } else {  // single buffer: the only batch in flight
-          __pipeline_wait_prior(0);
-          __syncthreads();
+  const int nt = J.nt;
+  const int nsteps = ((nx + G::ROWS - 1) / G::ROWS) * nt;
+  auto issue = [&](int k, int b) {
+    const int r0 = (k / nt) * G::ROWS, t = k - (k / nt) * nt;
+    const int nr = min(G::ROWS, nx - r0);
+    const Cx<T>* src = J.s[t] + ((int64_t)kz * P + x0 + r0) * L;  // nr contiguous rows
+    stg.begin(b, (uint32_t)(nr * L * sizeof(Cx<T>)));
+    stg.rows(slab + b * G::SLAB, LS, src, L, nr, L, b);
+  };
+  if (nsteps > 0) issue(0, 0);
+  stg.commit();
+  Cx<T> yacc[S::R2];
+  for (int k = 0; k < nsteps; ++k) {
+    const int b = k & 1;
+    if (k + 1 < nsteps) issue(k + 1, b ^ 1);
+    stg.commit();
+    stg.wait(b);
+    const int r0 = (k / nt) * G::ROWS, t = k - (k / nt) * nt;
+    const int nr = min(G::ROWS, nx - r0);
+    const int nl = min(LPW, nr - wl0);
+    if (nl > 0) {
+      const int ax = J.yax[t];
+      const Cx<T>* sl = slab + b * G::SLAB + wl0 * LS;
+      auto load = [&](int line, int y, int) -> Cx<T> { return sl[line * LS + y]; };
+      auto store = [&](int line, int q, int k2, Cx<T> v) {
+        const int iy = bin_to_index(q, L, K1, B1);
+        if (iy >= 0) {
+          if (ax == 1) v = mul_ik<T>(v, (T)(kTwoPi * (double)freq_of(iy, K1, B1)));
+          else if (ax == 2) v = mul_ik<T>(v, kzk);
         }
-        const int nl = min(LPW, nr - wl0);
-        if (nl > 0) {
-          const int ax = J.yax[t];
-          const Cx<T>* sl = slab + wl0 * LS;
-          auto load = [&](int line, int y, int) -> Cx<T> { return sl[line * LS + y]; };
-          auto store = [&](int line, int q, int, Cx<T> v) {
-            const int iy = bin_to_index(q, L, K1, B1);
-            if (iy < 0) return;
-            if (ax == 1) v = mul_ik<T>(v, (T)(kTwoPi * (double)freq_of(iy, K1, B1)));
-            else if (ax == 2) v = mul_ik<T>(v, kzk);
-            Cx<T>* rp = Ij + (size_t)iy * XLP + r0 + wl0 + line;  // owned by this lane for every term
-            BLR_CHECK(r0 + wl0 + line < XL && iy < B1, "fwd2 Ipl");
-            *rp = t == 0 ? v : cadd(*rp, v);
-          };
-          wfft<T, S, false, true>(slab + wl0 * LS, tw, nl, load, store);
+        yacc[k2] = t == 0 ? v : cadd(yacc[k2], v);
+        if (t == nt - 1 && iy >= 0) {  // this round's sum is complete: push it to the owner
+          const int qo = iy / KYL, l = iy - (iy / KYL) * KYL;
+          BLR_CHECK(qo < kF2Cl && x0 + r0 + wl0 + line < P, "fwd2 push");
+          rem[qo][(size_t)l * XP + x0 + r0 + wl0 + line] = yacc[k2];
         }
-        __syncthreads();  // slab reuse
-      }
+      };
+      wfft<T, S, false, true>(slab + b * G::SLAB + wl0 * LS, tw, nl, load, store);
     }
+    __syncthreads();  // buffer b is refilled by step k + 2
   }
-  cluster.sync();  // every CTA's I slice complete and visible cluster-wide
+  cluster.sync();  // every CTA's pushes complete and visible
 
-  // ---- phase 2: forward x FFTs of this CTA's ky lines (inputs over DSMEM) ----
-  Cx<T>* rem[kF2Cl];
-#pragma unroll
-  for (int q = 0; q < kF2Cl; ++q) rem[q] = cluster.map_shared_rank(Ipl, q);
+  // ---- phase 2: forward x FFTs of this CTA's ky lines (local I) ----
   Cx<T>* tile = slab + warp * TileG<T, S>::TILE;
+  Cx<T>* res = slab + kF2W * TileG<T, S>::TILE;  // [B0][KYLP]
+  const int xax = J.xax;
   for (int l0 = 0; l0 < nky; l0 += kF2W * LPW) {
     const int nl = min(LPW, nky - l0 - wl0);
     if (nl > 0) {
-      for (int j = 0; j < nj; ++j) {
-        const int xax = a.job[o][j].xax;
-        const size_t joff = (size_t)j * B1 * XLP;
-        auto load = [&](int line, int x, int) -> Cx<T> {
-          const int q = x / XL, xl = x - (x / XL) * XL;
-          BLR_CHECK(q < kF2Cl && ky0 + l0 + wl0 + line < B1, "fwd2 dsmem");
-          return rem[q][joff + (size_t)(ky0 + l0 + wl0 + line) * XLP + xl];
-        };
-        auto store = [&](int line, int qb, int, Cx<T> v) {
-          const int ix = bin_to_index(qb, L, K0, B0);
-          if (ix < 0) return;
-          if (xax == 0) v = mul_ik<T>(v, (T)(kTwoPi * (double)freq_of(ix, K0, B0)));
-          Cx<T>* rp = res + (size_t)ix * KYLP + l0 + wl0 + line;  // owned by this lane for every job
-          BLR_CHECK(l0 + wl0 + line < KYL, "fwd2 res");
-          *rp = j == 0 ? v : cadd(*rp, v);
-        };
-        wfft<T, S, false>(tile, tw, nl, load, store);
-      }
+      auto load = [&](int line, int x, int) -> Cx<T> { return Iown[(size_t)(l0 + wl0 + line) * XP + x]; };
+      auto store = [&](int line, int qb, int, Cx<T> v) {
+        const int ix = bin_to_index(qb, L, K0, B0);
+        if (ix < 0) return;
+        if (xax == 0) v = mul_ik<T>(v, (T)(kTwoPi * (double)freq_of(ix, K0, B0)));
+        BLR_CHECK(l0 + wl0 + line < KYL, "fwd2 res");
+        res[(size_t)ix * KYLP + l0 + wl0 + line] = v;
+      };
+      wfft<T, S, false>(tile, tw, nl, load, store);
     }
   }
   __syncthreads();
   if (kz == 0) {
     // Hermitian symmetrization of the kz = 0 plane (reference symmetrize):
     // h(kx, ky) <- (h(kx, ky) + conj(h(-kx, -ky))) / 2; the mirror ky line may
-    // belong to another CTA of the cluster
-    cluster.sync();  // every CTA's res complete
+    // belong to another CTA of the cluster (its res, read over DSMEM)
+    cluster.sync();
     Cx<T>* rres[kF2Cl];
 #pragma unroll
     for (int q = 0; q < kF2Cl; ++q) rres[q] = cluster.map_shared_rank(res, q);
-    Cx<T>* sym = slab;  // [B0][KYLP], the slab is free now
+    Cx<T>* sym = Iown;  // [B0][KYLP] (I is consumed; B0 * KYLP <= KYL * XP)
     for (int i = threadIdx.x; i < B0 * nky; i += blockDim.x) {
       const int ix = i / nky, l = i - (i / nky) * nky;
       const int iy = ky0 + l;
       const int mix = ix == 0 ? 0 : B0 - ix, miy = iy == 0 ? 0 : B1 - iy;
       const int mq = miy / KYL, ml = miy - (miy / KYL) * KYL;
-      BLR_CHECK(mq < kF2Cl && (size_t)ix * KYLP + l < (size_t)G::SLAB, "fwd2 mirror");
+      BLR_CHECK(mq < kF2Cl, "fwd2 mirror");
       const Cx<T> p = res[(size_t)ix * KYLP + l], m = rres[mq][(size_t)mix * KYLP + ml];
       sym[(size_t)ix * KYLP + l] = cx<T>((T)0.5 * a.e.scale * (p.x + m.x), (T)0.5 * a.e.scale * (p.y - m.y));
     }
@@ -257,12 +259,13 @@ __global__ void __launch_bounds__(kF2W * 32) k_fwd2(Fwd2Args<T> a, PadGeom g, in
       return true;
     });
   }
-  cluster.sync();  // no CTA exits while a peer may still read its shared memory
 }
 
 template <typename T, class S>
 bool fwd2_fits(const PadGeom& g) {
-  return (size_t)Fwd2Geom<T, S>::SLAB >= (size_t)g.B[0] * Fwd2Geom<T, S>::kylp(g.B[1]);
+  using G = Fwd2Geom<T, S>;
+  return 2 * (size_t)G::SLAB >= (size_t)kF2W * TileG<T, S>::TILE + (size_t)g.B[0] * G::kylp(g.B[1]) &&
+         (size_t)G::kyl(g.B[1]) * G::xp(g.P[0]) >= (size_t)g.B[0] * G::kylp(g.B[1]);
 }
 
 template <typename T, class S>

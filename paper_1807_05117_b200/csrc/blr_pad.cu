@@ -363,7 +363,7 @@ static void fwd2d(blr_ctx* c, PadEngine* e, const std::vector<FwdSpec<T>>& outs,
     }
   }
   bool fused = dispatch_fwd2<T>(c, e, Fwd2Args<T>{}, 0, 0, false);
-  for (size_t i = 0; i < outs.size() && fused; ++i) fused = xt[i].nt <= kF2MaxJobs;
+  for (size_t i = 0; i < outs.size() && fused; ++i) fused = xt[i].nt == 1;  // single-job outputs
   if (fused) {
     for (size_t off = 0; off < outs.size(); off += kMaxFwd) {
       Fwd2Args<T> a;
