@@ -571,11 +571,18 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
   const int nreal = OP == kOpContract ? a.d : (Tr::acc || OP == kOpRealize) ? 0 : ns_blk;
   // shared layout: tw | per warp { tile | stage[max(2*2*Kz1*LPW, LPW*L)] (xbuf aliases it after the
   //                                 C2R phase) | Vst[nst][LPW*L] | Rsm[nreal][LPW*L] }
-  const int fstride = Kz1 * S::LPW;  // per-field stage: Kz1 spectra rows
-  const int zoff = 4 * fstride;       // one zero row shared by both buffers and fields
+  // BLR_ZROW=1: each field's stage region ends with its own zero row, so the
+  // Hermitian gather indexes out-of-band rows with the in-band arithmetic (no
+  // select); A/B (r02): the outer op loses a CTA per SM to the extra rows
+  // (2.14 -> 2.31 ms), so the default keeps one shared zero row after them
+#ifndef BLR_ZROW
+#define BLR_ZROW 0
+#endif
+  const int fstride = (Kz1 + BLR_ZROW) * S::LPW;  // per-field stage: Kz1 spectra rows (+ zero row)
+  const int zoff = 4 * fstride;                   // shared zero row (BLR_ZROW=0) / end of regions
   using ZG = ZLineG<T, S>;
   constexpr int LX = ZG::LX, LR = ZG::LR;
-  const int stage_n = max(zoff + S::LPW, S::LPW * LX);
+  const int stage_n = max(zoff + (BLR_ZROW ? 0 : S::LPW), S::LPW * LX);  // must match launch_lines
   const int nst = Tr::acc ? a.nst : 0;
   const size_t warp_bytes = sizeof(Cx<T>) * ((size_t)TileG<T, S>::TILE + stage_n) +
                             sizeof(T) * (size_t)(nreal + nst) * S::LPW * LR;
@@ -647,7 +654,7 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
 #pragma unroll
     for (int n1 = 0; n1 < S::R1; ++n1) {
       const int k = S::R2 * n1 + n2;
-      int row = -1, sgn = 1;  // out of band: the shared zero row
+      int row = BLR_ZROW ? Kz1 : -1, sgn = 1;  // out of band: a zero row
       if (k == 0) { row = 0; sgn = 0; }
       else if (k <= K2) { row = k; sgn = 1; }
       else if (k >= L - K2) { row = L - k; sgn = -1; }
@@ -656,11 +663,29 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
     }
   }
   // the shared zero row (never overwritten by the prefetch)
-  if (lane < S::LPW) stage[zoff + lane] = cx<T>(0, 0);
+  if (BLR_ZROW) {
+    if (lane < 4 * S::LPW) stage[(lane / S::LPW) * fstride + Kz1 * S::LPW + lane % S::LPW] = cx<T>(0, 0);
+  } else if (lane < S::LPW) {
+    stage[zoff + lane] = cx<T>(0, 0);
+  }
   const int npair = (ns_blk + 1) / 2;
   const int nloop = OP == kOpContract ? a.n_nodes : 1;
   const int total = nloop * npair;
   // prefetch spectra of pair index q (node-major) into stage buffer q & 1
+  // per-lane element offsets of the spectra gather, fixed across fields and
+  // pairs: slot j covers stage entry i = lane + 32 j -> (row k, line l), global
+  // offset k * kzs + l (32-bit: Kz1 * P0 * P1 < 2^31); -1 marks an empty slot
+#ifndef BLR_PF_OFFS
+#define BLR_PF_OFFS 1
+#endif
+  constexpr int kPfSlots = BLR_PF_OFFS ? (S::LPW * (S::L / 2 + 1) + 31) / 32 : 1;  // >= Kz1 * LPW / 32
+  int pf_off[kPfSlots];
+#pragma unroll
+  for (int j = 0; j < kPfSlots; ++j) {
+    const int i = lane + 32 * j;
+    const int k = i / S::LPW, l = i - (i / S::LPW) * S::LPW;  // compile-time divisor
+    pf_off[j] = (i < Kz1 * S::LPW && l < nl) ? k * (int)kzs + l : -1;
+  }
   auto prefetch = [&](int q) {
     const int node = q / npair, p = q - node * npair;
     const int64_t noff = OP == kOpContract ? node * a.sin_node_stride : 0;
@@ -672,12 +697,19 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
         break;
       }
       const Cx<T>* src = a.sin[f] + noff + sline;
+#if BLR_PF_OFFS
+#pragma unroll
+      for (int j = 0; j < kPfSlots; ++j) {
+        if (pf_off[j] >= 0) __pipeline_memcpy_async(st + ff * fstride + lane + 32 * j, src + pf_off[j], sizeof(Cx<T>));
+        BLR_CHECK(pf_off[j] < 0 || ((q & 1) * 2 * fstride + ff * fstride + lane + 32 * j < zoff &&
+                                    sline + pf_off[j] < g.ns), "zlines sin");
+      }
+#else
       for (int i = lane; i < Kz1 * S::LPW; i += 32) {
         const int k = i / S::LPW, l = i - (i / S::LPW) * S::LPW;  // compile-time divisor
         if (l < nl) __pipeline_memcpy_async(st + ff * fstride + i, src + k * kzs + l, sizeof(Cx<T>));
-        BLR_CHECK((q & 1) * 2 * fstride + ff * fstride + i < zoff, "zlines stage");
-        BLR_CHECK(l >= nl || sline + k * kzs + l < g.ns, "zlines sin");
       }
+#endif
     }
     __pipeline_commit();
   };
@@ -730,6 +762,9 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
           const int jc = j < d ? j : 0;
+          // (masking absent components here would wait for the load before the
+          // FFT it is meant to overlap: A/B r02 map_tc 2.72 -> 2.90 ms; the
+          // mask stays at the use)
           dbuf[u][j] = __ldg(a.rin[dd + d + jc] + base + S::R1 * k2);
 #pragma unroll
           for (int o = 0; o < 3; ++o) dbuf[u][3 + 3 * o + j] = __ldg(a.rin[(o < d ? o : 0) * d + jc] + base + S::R1 * k2);
@@ -810,8 +845,8 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
       // branch-free Hermitian packing of F1 + i F2 (zero rows index the zero pad row)
       const int h = hidx[n1];
       BLR_CHECK((h >= 0 ? st2o + h : zoff) + line < stage_n, "zlines gather");
-      const Cx<T> F1 = stage[(h >= 0 ? st1o + h : zoff) + line];
-      const Cx<T> F2 = stage[(h >= 0 ? st2o + h : zoff) + line];
+      const Cx<T> F1 = stage[(BLR_ZROW || h >= 0 ? st1o + h : zoff) + line];
+      const Cx<T> F2 = stage[(BLR_ZROW || h >= 0 ? st2o + h : zoff) + line];
       const T sg = (T)hsg[n1];
       return cx<T>(F1.x - sg * F2.y, sg * F1.y + F2.x);
     };
@@ -1576,7 +1611,8 @@ void launch_lines(blr_ctx* c, PadEngine* e, const LineArgs<T>& a) {
   const int ns_blk = OP == kOpContract ? a.d : a.ns;
   const int nreal = OP == kOpContract ? a.d : (ZOp<OP>::acc || OP == kOpRealize) ? 0 : ns_blk;
   const int nst = ZOp<OP>::acc ? a.nst : 0;
-  const size_t stage_n = std::max<size_t>(4 * (size_t)g.Kz1 * S::LPW + S::LPW, (size_t)S::LPW * ZLineG<T, S>::LX);
+  const size_t stage_n = std::max<size_t>(BLR_ZROW ? 4 * (size_t)(g.Kz1 + 1) * S::LPW : 4 * (size_t)g.Kz1 * S::LPW + S::LPW,
+                                          (size_t)S::LPW * ZLineG<T, S>::LX);
   const size_t warp_bytes = sizeof(Cx<T>) * ((size_t)TileG<T, S>::TILE + stage_n) +
                             sizeof(T) * (size_t)(nreal + nst) * S::LPW * ZLineG<T, S>::LR;
   const bool twg = sizeof(T) == 8 && !(ZOp<OP>::acc && OP != kOpContract);  // as kTwG in the kernel
