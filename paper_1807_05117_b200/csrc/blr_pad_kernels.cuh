@@ -1003,10 +1003,15 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
 #pragma unroll
         for (int k2 = 0; k2 < S::R2; ++k2) {
           T v1 = 0, v2 = 0;
+          if constexpr (OS >= 100) {  // compile-time output pair (OS - 100, OS - 99)
+            v1 = acc[OS - 100][k2];
+            if constexpr (OS - 99 < NOM) v2 = acc[OS - 99][k2];
+          } else {
 #pragma unroll
-          for (int q = 0; q < NOM; ++q) {
-            if (q == o) v1 = acc[q][k2];
-            if (q == o + 1) v2 = acc[q][k2];
+            for (int q = 0; q < NOM; ++q) {
+              if (q == o) v1 = acc[q][k2];
+              if (q == o + 1) v2 = acc[q][k2];
+            }
           }
           BLR_CHECK(bl * LX + k1 + S::R1 * k2 < stage_n, "zlines xbuf acc");
           xbuf[bl * LX + k1 + S::R1 * k2] = cx<T>(v1, v2);
@@ -1022,7 +1027,7 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
     auto load = [&](int line, int z, int n1) -> Cx<T> {
       if constexpr (Tr::acc) {
         return xbuf[line * LX + z];
-      } else if constexpr (OP == kOpOuter && OS >= 0) {
+      } else if constexpr (OP == kOpOuter && OS >= 0 && OS < 100) {
         constexpr int I1 = OS / 3, J1 = OS % 3, I2 = (OS + 1) / 3, J2 = (OS + 1) % 3;
         return cx<T>(rreg[I1][n1] * vreg[J1][n1], OS + 1 < 9 ? rreg[I2 < 3 ? I2 : 0][n1] * vreg[J2][n1] : (T)0);
       } else if constexpr (OP == kOpOuter) {
@@ -1044,18 +1049,50 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
     wfft<T, S, false>(tile, twp, nl, load, store);
     Cx<T>* O1 = a.sout[o] + sline;
     Cx<T>* O2 = two ? a.sout[o + 1] + sline : nullptr;
-    for (int idx = lane; idx < S::LPW * Kz1; idx += 32) {
-      const int k = idx / S::LPW, l = idx - (idx / S::LPW) * S::LPW;  // compile-time divisor
-      if (l >= nl) continue;
-      BLR_CHECK(sline + k * kzs + l < g.ns && l * LX + k < stage_n, "zlines out");
-      const Cx<T> Z = xbuf[l * LX + k];
-      Cx<T> Zm = xbuf[l * LX + (k == 0 ? 0 : L - k)];
-      Zm.y = -Zm.y;
-      O1[k * kzs + l] = cx<T>((T)0.5 * (Z.x + Zm.x), (T)0.5 * (Z.y + Zm.y));
-      if (two) O2[k * kzs + l] = cx<T>((T)0.5 * (Z.y - Zm.y), (T)-0.5 * (Z.x - Zm.x));
+// A/B (r02): the fixed-trip extraction is -1.4% on the deformation GN HVP
+// (9.64 -> 9.51 ms); compile-time ACC output slots (BLR_ZOUT_UNROLL) +1.4%
+#ifndef BLR_ZEXT_UNROLL
+#define BLR_ZEXT_UNROLL 1
+#endif
+    if constexpr (BLR_ZEXT_UNROLL && BLR_PF_OFFS) {
+      // fixed-trip extraction over the prefetch slots (same (k, l) mapping and
+      // global offsets): all shared loads of the warp's rows can be in flight
+      Cx<T> Zs[kPfSlots], Zms[kPfSlots];
+#pragma unroll
+      for (int j = 0; j < kPfSlots; ++j) {
+        const int idx = lane + 32 * j;
+        const int k = idx / S::LPW, l = idx - (idx / S::LPW) * S::LPW;
+        const int kk = pf_off[j] >= 0 ? k : 0, ll = pf_off[j] >= 0 ? l : 0;
+        Zs[j] = xbuf[ll * LX + kk];
+        Zms[j] = xbuf[ll * LX + (kk == 0 ? 0 : L - kk)];
+      }
+#pragma unroll
+      for (int j = 0; j < kPfSlots; ++j) {
+        if (pf_off[j] < 0) continue;
+        const Cx<T> Z = Zs[j];
+        Cx<T> Zm = Zms[j];
+        Zm.y = -Zm.y;
+        O1[pf_off[j]] = cx<T>((T)0.5 * (Z.x + Zm.x), (T)0.5 * (Z.y + Zm.y));
+        if (two) O2[pf_off[j]] = cx<T>((T)0.5 * (Z.y - Zm.y), (T)-0.5 * (Z.x - Zm.x));
+      }
+    } else {
+      for (int idx = lane; idx < S::LPW * Kz1; idx += 32) {
+        const int k = idx / S::LPW, l = idx - (idx / S::LPW) * S::LPW;  // compile-time divisor
+        if (l >= nl) continue;
+        BLR_CHECK(sline + k * kzs + l < g.ns && l * LX + k < stage_n, "zlines out");
+        const Cx<T> Z = xbuf[l * LX + k];
+        Cx<T> Zm = xbuf[l * LX + (k == 0 ? 0 : L - k)];
+        Zm.y = -Zm.y;
+        O1[k * kzs + l] = cx<T>((T)0.5 * (Z.x + Zm.x), (T)0.5 * (Z.y + Zm.y));
+        if (two) O2[k * kzs + l] = cx<T>((T)0.5 * (Z.y - Zm.y), (T)-0.5 * (Z.x - Zm.x));
+      }
     }
     __syncwarp();
   };
+#ifndef BLR_ZOUT_UNROLL
+#define BLR_ZOUT_UNROLL 0
+#endif
+  constexpr bool kUnrollAccOut = BLR_ZOUT_UNROLL && Tr::acc && OP != kOpContract && NOM == 3;
   if (outer3) {
     if constexpr (kUnrollOuter) {
       out_step(0, std::integral_constant<int, 0>{});
@@ -1063,6 +1100,11 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
       out_step(4, std::integral_constant<int, 4>{});
       out_step(6, std::integral_constant<int, 6>{});
       out_step(8, std::integral_constant<int, 8>{});
+    }
+  } else if (kUnrollAccOut && no == 3) {
+    if constexpr (kUnrollAccOut) {  // compile-time output slots: no selects over the accumulators
+      out_step(0, std::integral_constant<int, 100>{});
+      out_step(2, std::integral_constant<int, 102>{});
     }
   } else {
     for (int o = 0; o < no; o += 2) out_step(o, std::integral_constant<int, -1>{});
