@@ -441,11 +441,10 @@ template <int OP> struct ZOp {
 
 constexpr int kZWarps = 2;
 // Occupancy targets (CTAs per SM) of the z-line kernel per op; 0 = registers
-// unconstrained.  A/B (r02): the unrolled outer op (rho / V operands in
-// registers, BLR_ZUNROLL_OUTER=1) at 6 CTAs per SM spills and ties the default,
-// at 5 it is 2% slower; both stay off.
+// unconstrained.  The outer op is held at 6 CTAs per SM (its shared-memory
+// limit; see BLR_ZUNROLL_OUTER).
 #ifndef BLR_ZMINB_OUTER
-#define BLR_ZMINB_OUTER 0
+#define BLR_ZMINB_OUTER 6
 #endif
 #ifndef BLR_ZMINB_MAPTC
 #define BLR_ZMINB_MAPTC 0
@@ -964,13 +963,19 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
   // Outer (3-D, unrolled): rho_i at this lane's step-A positions, read once from
   // Rsm into registers for all nine products (instead of two shared loads per
   // element per output pair)
+// Outer op: 1 = compile-time products with rho in registers (rreg), 2 = the
+// same with rho read from shared memory, 0 = runtime output loop.  A/B (r02):
+// 2 with 6 CTAs/SM: outer z-lines 2.13 -> 1.90 ms, deformation GN HVP 9.52 ->
+// 9.31 ms (1 spills at 6 CTAs/SM and ties 0)
 #ifndef BLR_ZUNROLL_OUTER
-#define BLR_ZUNROLL_OUTER 0
+#define BLR_ZUNROLL_OUTER 2
 #endif
   constexpr bool kUnrollOuter = BLR_ZUNROLL_OUTER != 0 && OP == kOpOuter;
-  T rreg[kUnrollOuter ? 3 : 1][kUnrollOuter ? S::R1 : 1];
+  // BLR_ZUNROLL_OUTER=2: compile-time products but rho read from Rsm (no rreg)
+  constexpr bool kOuterRreg = BLR_ZUNROLL_OUTER == 1;
+  T rreg[kUnrollOuter && kOuterRreg ? 3 : 1][kUnrollOuter && kOuterRreg ? S::R1 : 1];
   const bool outer3 = kUnrollOuter && a.d == 3 && no == 9;
-  if constexpr (kUnrollOuter) {
+  if constexpr (kUnrollOuter && kOuterRreg) {
     if (outer3) {
       __syncwarp();
       const int la = lane / S::R2, n2a = lane - (lane / S::R2) * S::R2;
@@ -1029,7 +1034,13 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
         return xbuf[line * LX + z];
       } else if constexpr (OP == kOpOuter && OS >= 0 && OS < 100) {
         constexpr int I1 = OS / 3, J1 = OS % 3, I2 = (OS + 1) / 3, J2 = (OS + 1) % 3;
-        return cx<T>(rreg[I1][n1] * vreg[J1][n1], OS + 1 < 9 ? rreg[I2 < 3 ? I2 : 0][n1] * vreg[J2][n1] : (T)0);
+        if constexpr (kOuterRreg) {
+          return cx<T>(rreg[I1][n1] * vreg[J1][n1], OS + 1 < 9 ? rreg[I2 < 3 ? I2 : 0][n1] * vreg[J2][n1] : (T)0);
+        } else {
+          const int li = line * LR + z;
+          return cx<T>(Rsm[I1 * ldR + li] * vreg[J1][n1],
+                       OS + 1 < 9 ? Rsm[(I2 < 3 ? I2 : 0) * ldR + li] * vreg[J2][n1] : (T)0);
+        }
       } else if constexpr (OP == kOpOuter) {
         const int li = line * LR + z;
         const T v1 = oj1 == 0 ? vreg[0][n1] : (oj1 == 1 ? vreg[1][n1] : vreg[2][n1]);
