@@ -748,6 +748,13 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
   // loads are issued before that pair's transform and consumed after it, so
   // the D(u) / dv reads overlap FFT work instead of stalling the kernel start.
   // Absent components (d < 3) read component 0 and are masked.
+// Rotating accumulators (BLR_ZROT=1): A/B (r02) map_tc 2.70 -> 3.12 ms (the
+// rotations' register moves and a longer live range), so off
+#ifndef BLR_ZROT
+#define BLR_ZROT 0
+#endif
+  constexpr bool kRotOp = BLR_ZROT && (OP == kOpMap || OP == kOpMapTC);
+  const bool rot = kRotOp && a.d == 3 && ns_blk == 9;
   // MapTQ: the same chunked schedule for acc_i += q_i, q = Du . dV precomputed
   // (rin: V [0,d) q [d,2d)): 3 loads per position instead of 12.
   constexpr int DCH = (S::R2 + 4) / 5;  // k2 columns per chunk
@@ -791,6 +798,8 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
   };
   auto du_acc = [&](auto cc) {
     constexpr int c = decltype(cc)::value;
+    // rotations done before pair c (3-D Map / MapTC order: after pairs 1, 2, 4)
+    constexpr int RC = c >= 3 ? 2 : (c >= 2 ? 1 : 0);
     if constexpr (OP == kOpMapTQ) {
       const int d = a.d;
 #pragma unroll
@@ -811,6 +820,12 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
           T sdu = 0;
 #pragma unroll
           for (int j = 0; j < 3; ++j) sdu += (j < d ? dbuf[u][3 + 3 * (o < 3 ? o : 0) + j] : (T)0) * dbuf[u][j];
+          if constexpr (kRotOp && NOM == 3) {
+            if (rot) {
+              acc[(o - RC + 3) % 3][k2] += sdu;
+              continue;
+            }
+          }
           acc[o][k2] += sdu;
         }
       }
@@ -847,6 +862,10 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
     T c1[NOM], c2[NOM];
     const T* V1 = Vst;
     const T* V2 = Vst;
+    // rotating accumulators (3-D Map / MapTC): the output being filled always
+    // sits in acc[0]; a pair adds to acc[0] (and, when it straddles two
+    // outputs, acc[1]) -- 2 FMAs per realized value instead of 6
+    const bool split = rot && (f + 1) / 3 != f / 3 && two;
     if constexpr (Tr::acc && OP != kOpContract && QS < 0) {
       const int o1 = a.oi[f], o2 = two ? a.oi[f + 1] : -1;
       const T sg1 = (T)a.sg[f], sg2 = two ? (T)a.sg[f + 1] : (T)0;
@@ -894,6 +913,13 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
         }
         const T p1 = v.x * V1[li];
         const T p2 = v.y * V2[li];
+        if constexpr (kRotOp) {
+          if (rot) {
+            acc[0][k2] += p1 + (split ? (T)0 : p2);
+            acc[1][k2] += split ? p2 : (T)0;
+            return;
+          }
+        }
 #pragma unroll
         for (int o = 0; o < NOM; ++o) acc[o][k2] += c1[o] * p1 + c2[o] * p2;
       }
@@ -906,6 +932,17 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
     if constexpr (kDu) {
       if constexpr (QS >= 0) du_acc(std::integral_constant<int, QS>{});
       else du_chunk(q, du_acc);
+    }
+    if constexpr (kRotOp && NOM == 3) {
+      if (rot && (f % 3 == 2 || (two && (f + 1) % 3 == 2))) {  // an output completed: rotate
+#pragma unroll
+        for (int k2 = 0; k2 < S::R2; ++k2) {
+          const T t0 = acc[0][k2];
+          acc[0][k2] = acc[1][k2];
+          acc[1][k2] = acc[2][k2];
+          acc[2][k2] = t0;
+        }
+      }
     }
     if constexpr (OP == kOpContract) {
       if (p == npair - 1) {
