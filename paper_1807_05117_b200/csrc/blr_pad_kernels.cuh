@@ -79,6 +79,29 @@ __device__ __forceinline__ bool load_tw_async(T* dst, const double* src, int L) 
 template <typename T>
 __device__ __forceinline__ Cx<T> mul_ik(Cx<T> z, T k) { return cx<T>(-(k * z.y), k * z.x); }
 
+// Per-lane step-A gather table of an inverse pass: lane (line, n2) reads grid
+// bin q = R2 n1 + n2 for n1 = 0..R1-1; off[n1] = band index * stride (or -1
+// outside the band), kk[n1] = 2 pi k of that band index.  Built once per CTA
+// instead of per element (bin_to_index / freq_of / int->fp64 per gathered value).
+// A/B (r02): neutral (y-inverse 1.47 vs 1.45 ms), so off.
+#ifndef BLR_PASS_TABLES
+#define BLR_PASS_TABLES 0
+#endif
+template <typename T, class S>
+struct GatherTab {
+  int off[S::R1];
+  T kk[S::R1];
+  __device__ __forceinline__ void build(int K, int B, int stride) {
+    const int n2 = (threadIdx.x & 31) % S::R2;
+#pragma unroll
+    for (int n1 = 0; n1 < S::R1; ++n1) {
+      const int b = bin_to_index(S::R2 * n1 + n2, S::L, K, B);
+      off[n1] = b >= 0 ? b * stride : -1;
+      kk[n1] = (T)(kTwoPi * (double)freq_of(b >= 0 ? b : 0, K, B));
+    }
+  }
+};
+
 // ---------------------------------------------------------------------------
 // inverse x pass: band H [kz][kx][ky] -> I [xf][kz][ky][x]
 // ---------------------------------------------------------------------------
@@ -298,7 +321,17 @@ __global__ void __launch_bounds__(kPW * 32) k_xinv(XPassArgs<T> a, PadGeom g, co
     BLR_CHECK(((int64_t)kz * B1 + cky0 + wl0 + line) * S::L + x < g.n1, "xinv out");
     out[line * S::L + x] = v;
   };
-  if (mulx) {  // uniform per CTA: two gathers instead of a per-element branch
+  if (BLR_PASS_TABLES) {
+    GatherTab<T, S> tb;
+    tb.build(K0, B0, LPCS);
+    auto load = [&](int line, int, int n1) -> Cx<T> {
+      const int o = tb.off[n1];
+      Cx<T> z = sl[(o >= 0 ? o : 0) + line];
+      if (mulx) z = mul_ik<T>(z, tb.kk[n1]);
+      return o >= 0 ? z : cx<T>(0, 0);
+    };
+    wfft<T, S, true>(tile, tw, nl, load, store);
+  } else if (mulx) {  // uniform per CTA: two gathers instead of a per-element branch
     auto load = [&](int line, int p, int) -> Cx<T> {
       const int ix = bin_to_index(p, S::L, K0, B0);
       const int ixc = ix >= 0 ? ix : 0;
@@ -386,7 +419,37 @@ __global__ void __launch_bounds__(kPW * 32) k_yinv(YPassArgs<T> a, PadGeom g, co
     BLR_CHECK(((int64_t)kz * P0 + cx0 + wl0 + line) * S::L + y < g.ns, "yinv out");
     out[line * S::L + y] = v;
   };
-  if (nt == 1) {
+  if (BLR_PASS_TABLES) {
+    GatherTab<T, S> tb;
+    tb.build(K1, B1, LPCS);
+    if (nt == 1) {
+      const int ax0 = ax[0];
+      const T m0 = ax0 == 2 ? kzk : (T)0;
+      const Cx<T>* sl = slab + wl0;
+      auto load1 = [&](int line, int, int n1) -> Cx<T> {
+        const int o = tb.off[n1];
+        Cx<T> z = sl[(o >= 0 ? o : 0) + line];
+        if (ax0 >= 1) z = mul_ik<T>(z, ax0 == 1 ? tb.kk[n1] : m0);
+        return o >= 0 ? z : cx<T>(0, 0);
+      };
+      wfft<T, S, true>(tile, tw, nl, load1, store);
+    } else {
+      auto loadn = [&](int line, int, int n1) -> Cx<T> {
+        const int o = tb.off[n1];
+        const int oc = o >= 0 ? o : 0;
+        Cx<T> acc = cx<T>(0, 0);
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          if (ax[t] < -1) break;
+          Cx<T> z = slab[t * B1 * LPCS + oc + wl0 + line];
+          if (ax[t] >= 1) z = mul_ik<T>(z, ax[t] == 1 ? tb.kk[n1] : kzk);
+          acc = cadd(acc, z);
+        }
+        return o >= 0 ? acc : cx<T>(0, 0);
+      };
+      wfft<T, S, true>(tile, tw, nl, loadn, store);
+    }
+  } else if (nt == 1) {
     // single-term output (the common case): no term loop in the gather
     const int ax0 = ax[0];
     const Cx<T>* sl = slab + wl0;
