@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--registration", type=int, default=1, help="also time one full GN registration")
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--profile-only", action="store_true", help="one instrumented HVP, no timing")
-    ap.add_argument("--in-flight", type=int, default=2,
+    ap.add_argument("--in-flight", type=int, default=1,
                     help="--batch: pairs registered concurrently per GPU (threads + streams)")
     ap.add_argument("--batch", type=int, default=0,
                     help="SURVEY config 5: register this many seeded pairs sharded over the ranks "

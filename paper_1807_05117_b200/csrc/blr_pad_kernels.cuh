@@ -758,7 +758,8 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
 #ifndef BLR_PF_OFFS
 #define BLR_PF_OFFS 1
 #endif
-  constexpr int kPfSlots = BLR_PF_OFFS ? (S::LPW * (S::L / 2 + 1) + 31) / 32 : 1;  // >= Kz1 * LPW / 32
+  // Kz1 = K + 1 <= (L - 1) / 3 + 1 since the pad satisfies L >= 3K + 1
+  constexpr int kPfSlots = BLR_PF_OFFS ? (S::LPW * ((S::L - 1) / 3 + 1) + 31) / 32 : 1;
   int pf_off[kPfSlots];
 #pragma unroll
   for (int j = 0; j < kPfSlots; ++j) {

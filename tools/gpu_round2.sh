@@ -6,7 +6,7 @@ python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2
 python bench.py > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err; echo "bench rc=$?"
 python bench.py --objective state --registration 0 --cpu-baseline 0 > gpurun_out/${T}_bench_state.json 2>> gpurun_out/${T}_bench.err
 python bench.py --dtype float32 --registration 0 --cpu-baseline 0 > gpurun_out/${T}_bench_f32.json 2>> gpurun_out/${T}_bench.err
-python bench.py --batch 64 --in-flight 2 > gpurun_out/${T}_bench_batch64.json 2>> gpurun_out/${T}_bench.err
+python bench.py --batch 64 > gpurun_out/${T}_bench_batch64.json 2>> gpurun_out/${T}_bench.err
 python bench.py --steps 2 --warmup 3 --registration 0 --cpu-baseline 0 > gpurun_out/${T}_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches.csv \
     python bench.py --steps 2 --warmup 3 --registration 0 --cpu-baseline 0 > gpurun_out/${T}_ncu_launch.log 2>&1; echo "launch list rc=$?"
