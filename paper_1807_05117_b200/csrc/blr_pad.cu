@@ -451,6 +451,13 @@ static void fwd2d(blr_ctx* c, PadEngine* e, const std::vector<FwdSpec<T>>& outs,
     a.cur = rk.cur ? (Cx<T>*)rk.cur + shift : nullptr;
     a.acc = rk.acc ? (Cx<T>*)rk.acc + shift : nullptr;
     a.stage = rk.stage ? (Cx<T>*)rk.stage + shift : nullptr;
+// BLR_XFWD_DEFER=1: the x pass writes its results and k_xfwd_epi applies the
+// epilogue (156 instead of 226 registers in the transform kernel).  A/B (r02):
+// x-forward 1.92 -> 2.04 ms per HVP, so off.
+#ifndef BLR_XFWD_DEFER
+#define BLR_XFWD_DEFER 0
+#endif
+    a.kres = BLR_XFWD_DEFER ? (Cx<T>*)e_scratch(c, e, 2, (size_t)a.no * g.nh * sizeof(Cx<T>)) : nullptr;
     {
       ProfScope ps(c, "pad_xpass_fwd", ((double)nterm * g.n1 + a.no * g.nh * (rk.s ? 4 : 2)) * sizeof(Cx<T>));
       dispatch_xfwd<T>(c, e, a);

@@ -819,6 +819,7 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
 #endif
   constexpr bool kRotOp = BLR_ZROT && (OP == kOpMap || OP == kOpMapTC);
   const bool rot = kRotOp && a.d == 3 && ns_blk == 9;
+  const bool sw3 = (OP == kOpMap || OP == kOpMapTC) && a.d == 3 && ns_blk == 9 && total == 5;
   // MapTQ: the same chunked schedule for acc_i += q_i, q = Du . dV precomputed
   // (rin: V [0,d) q [d,2d)): 3 loads per position instead of 12.
   constexpr int DCH = (S::R2 + 4) / 5;  // k2 columns per chunk
@@ -992,7 +993,47 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
       if constexpr (QS >= 0) du_issue(std::integral_constant<int, QS>{});
       else du_chunk(q, du_issue);
     }
-    wfft<T, S, true>(tile, twp, nl, load, store);
+// A/B (r02): neutral (9.17 vs 9.14 ms), so off
+#ifndef BLR_ZPAIRSW
+#define BLR_ZPAIRSW 0
+#endif
+    if constexpr (BLR_ZPAIRSW && (OP == kOpMap || OP == kOpMapTC) && QS < 0) {
+      if (sw3) {
+        // 3-D Map / MapTC: the DFT outputs stay in registers and a warp-uniform
+        // switch on the pair applies compile-time output / V slots (one FMA per
+        // realized value; the DFT is not duplicated)
+        wfft_a<T, S, true>(tile, twp, nl, load);
+        Cx<T> u[S::R2];
+        if (wfft_b_regs<T, S, true>(tile, nl, u)) {
+          auto apply = [&](auto pc) {
+            constexpr int PC = decltype(pc)::value;
+            constexpr int F1 = 2 * PC, F2 = 2 * PC + 1;
+#pragma unroll
+            for (int k2 = 0; k2 < S::R2; ++k2) {
+              const int li = bl * LR + k1 + S::R1 * k2;
+              if (OP == kOpMap && a.wout[F1]) {
+                const int64_t gi = rline + bl * L + k1 + S::R1 * k2;
+                a.wout[F1][gi] = u[k2].x;
+                if (F2 < 9) a.wout[F2][gi] = u[k2].y;
+              }
+              acc[F1 / 3][k2] += u[k2].x * Vst[(F1 % 3) * ldR + li];
+              if constexpr (F2 < 9) acc[F2 / 3][k2] += u[k2].y * Vst[(F2 % 3) * ldR + li];
+            }
+          };
+          switch (p) {
+            case 0: apply(std::integral_constant<int, 0>{}); break;
+            case 1: apply(std::integral_constant<int, 1>{}); break;
+            case 2: apply(std::integral_constant<int, 2>{}); break;
+            case 3: apply(std::integral_constant<int, 3>{}); break;
+            default: apply(std::integral_constant<int, 4>{}); break;
+          }
+        }
+      } else {
+        wfft<T, S, true>(tile, twp, nl, load, store);
+      }
+    } else {
+      wfft<T, S, true>(tile, twp, nl, load, store);
+    }
     if constexpr (kDu) {
       if constexpr (QS >= 0) du_acc(std::integral_constant<int, QS>{});
       else du_chunk(q, du_acc);
@@ -1369,6 +1410,7 @@ struct FwdArgs {
   Cx<T>* cur;
   Cx<T>* acc;
   Cx<T>* stage;
+  Cx<T>* kres;      // deferred epilogue: x-pass results [no][nh] (k_xfwd_epi consumes them)
 };
 
 // Cooperative epilogue of one (output, kz, ky-chunk) block from the result
@@ -1435,11 +1477,14 @@ __device__ __forceinline__ void epilogue_block(const FwdArgs<T>& a, const FwdOut
 // with its mirror -ky (warp 0: units p0.., warp 1: their mirrors), so the
 // Hermitian symmetrization of the kz = 0 plane (the reference's symmetrize)
 // happens inside the item: no separate fix-up kernel.
-template <typename T, class S>
 #ifndef BLR_XFWD_MINB
 #define BLR_XFWD_MINB 3
 #endif
-__global__ void __launch_bounds__(kPWF * 32, BLR_XFWD_MINB) k_xfwd(FwdArgs<T> a, PadGeom g, const double* __restrict__ twg) {
+// DEFER: the x pass only writes its (scaled, kz = 0 symmetrized) results to
+// a.kres; the RK4 / -(v + .) epilogue runs in k_xfwd_epi, a streaming kernel at
+// full occupancy, so the transform kernel carries no epilogue registers.
+template <typename T, class S, bool DEFER = false>
+__global__ void __launch_bounds__(kPWF * 32, DEFER ? 6 : BLR_XFWD_MINB) k_xfwd(FwdArgs<T> a, PadGeom g, const double* __restrict__ twg) {
   static_assert(kPWF == 2, "kz = 0 mirror items use one warp per half");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int LPW = S::LPW;
@@ -1544,7 +1589,7 @@ __global__ void __launch_bounds__(kPWF * 32, BLR_XFWD_MINB) k_xfwd(FwdArgs<T> a,
     if (ntt >= nt) { nit = it + gridDim.x; ntt = 0; }
     if (nit < nitems) issue(nit, ntt, b ^ 1);
     stg.commit();
-    if (t == 0) prefetch_epi(it);
+    if (!DEFER && t == 0) prefetch_epi(it);
     stg.wait(b);
     const Item m = decode(it - o * per);
     const int kz = m.kz;
@@ -1590,7 +1635,7 @@ __global__ void __launch_bounds__(kPWF * 32, BLR_XFWD_MINB) k_xfwd(FwdArgs<T> a,
         src = sym;
         sc = (T)1;
       }
-      epilogue_block<T, LPC>(a, O, o, g, [&](int ix, int l, int64_t& e, Cx<T>& r) {
+      auto elem = [&](int ix, int l, int64_t& e, Cx<T>& r) {
         int iy;
         if (kz > 0) {
           if (l >= m.c1) return false;
@@ -1602,7 +1647,17 @@ __global__ void __launch_bounds__(kPWF * 32, BLR_XFWD_MINB) k_xfwd(FwdArgs<T> a,
         e = ((int64_t)kz * B0 + ix) * B1 + iy;
         r = cscale(src[ix * LPCS + l], sc);
         return true;
-      });
+      };
+      if constexpr (DEFER) {
+        for (int i = threadIdx.x; i < B0 * LPC; i += blockDim.x) {
+          const int ix = i / LPC, l = i - (i / LPC) * LPC;  // compile-time divisor
+          int64_t e;
+          Cx<T> r;
+          if (elem(ix, l, e, r)) a.kres[(int64_t)o * g.nh + e] = r;
+        }
+      } else {
+        epilogue_block<T, LPC>(a, O, o, g, elem);
+      }
     }
     __syncthreads();
     it = nit;
@@ -1815,16 +1870,67 @@ void launch_yfwd(blr_ctx* c, PadEngine* e, const YFwdArgs<T>& a) {
   launch_pdl(k_yfwd<T, S>, grid, kPWF * 32, sm, c->stream, a, g, (const double*)e->tw[1]);
   BLR_LAUNCHED();
 }
+// the deferred x-pass epilogue: one thread per H-layout element of every output
+template <typename T>
+__global__ void __launch_bounds__(256) k_xfwd_epi(FwdArgs<T> a, PadGeom g) {
+  pdl_wait();
+  const int64_t n = (int64_t)a.no * g.nh;
+  const int s = a.rk_s;
+  for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < n; h += (int64_t)gridDim.x * blockDim.x) {
+    const int o = (int)(h / g.nh);
+    const int64_t e = h - (int64_t)o * g.nh;
+    const FwdOut<T>& O = a.o[o];
+    const Cx<T> r = a.kres[h];
+    Cx<T> k;
+    if (O.mode == kEpiNegAdd) {
+      const Cx<T> v = O.vt[e];
+      k = cx<T>(-(v.x + r.x), -(v.y + r.y));
+    } else if (O.mode == kEpiNeg) {
+      k = cx<T>(-r.x, -r.y);
+    } else {
+      k = r;
+    }
+    if (a.kout) a.kout[h] = k;
+    if (s) {
+      const Cx<T> cc = a.cur[h];
+      Cx<T> acv;
+      if (s == 1) {
+        acv = k;
+      } else {
+        const Cx<T> ac = a.acc[h];
+        const T m = s < 4 ? (T)2 : (T)1;
+        acv = cx<T>(ac.x + m * k.x, ac.y + m * k.y);
+      }
+      if (s < 4) {
+        a.acc[h] = acv;
+        a.stage[h] = cx<T>(cc.x + a.cs * k.x, cc.y + a.cs * k.y);
+      } else {
+        a.cur[h] = cx<T>(cc.x + a.h6 * acv.x, cc.y + a.h6 * acv.y);
+      }
+    }
+  }
+}
+
 template <typename T, class S>
 void launch_xfwd(blr_ctx* c, PadEngine* e, const FwdArgs<T>& a) {
   const PadGeom& g = e->g;
   constexpr int LPC = kPWF * S::LPW;
   const size_t sm = sizeof(Cx<T>) * (S::L + 2 * (size_t)LPC * row_stride<T, S, true>() +
                                      (size_t)g.B[0] * t_stride<LPC>());
-  ensure_smem(k_xfwd<T, S>, sm);
   const int nyb = (g.B[1] + LPC - 1) / LPC;
   const int n0 = (g.K[1] + 1 + S::LPW - 1) / S::LPW;
-  const int grid = persistent_grid(k_xfwd<T, S>, kPWF * 32, sm, a.no * (n0 + (g.Kz1 - 1) * nyb));
+  const int items = a.no * (n0 + (g.Kz1 - 1) * nyb);
+  if (a.kres) {
+    ensure_smem(k_xfwd<T, S, true>, sm);
+    const int grid = persistent_grid(k_xfwd<T, S, true>, kPWF * 32, sm, items);
+    launch_pdl(k_xfwd<T, S, true>, grid, kPWF * 32, sm, c->stream, a, g, (const double*)e->tw[0]);
+    BLR_LAUNCHED();
+    launch_pdl(k_xfwd_epi<T>, grid_blocks((int64_t)a.no * g.nh, 256, 148 * 8), 256, 0, c->stream, a, g);
+    BLR_LAUNCHED();
+    return;
+  }
+  ensure_smem(k_xfwd<T, S>, sm);
+  const int grid = persistent_grid(k_xfwd<T, S>, kPWF * 32, sm, items);
   launch_pdl(k_xfwd<T, S>, grid, kPWF * 32, sm, c->stream, a, g, (const double*)e->tw[0]);
   BLR_LAUNCHED();
 }
