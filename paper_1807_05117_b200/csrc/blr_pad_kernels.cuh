@@ -184,9 +184,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // padded smem rows; no per-element instructions); every thread then waits on
 // the mbarrier parity.  fp32 rows may be 8-byte aligned only: per-element
 // cp.async with commit / wait_group and a CTA barrier.
-template <typename T>
+template <typename T, bool BULK = sizeof(T) == 8>
 struct Stager {
-  static constexpr bool kBulk = sizeof(T) == 8;
+  static constexpr bool kBulk = BULK;
   uint64_t* bar;  // [2] in shared memory
   uint32_t phase;
   __device__ __forceinline__ void init(uint64_t* b) {
@@ -271,18 +271,33 @@ constexpr int phase_conflicts(int LS, int words) {
 }
 
 // ALIAS: the slab must also hold the warp's FFT tile over its own lines
-// (LS >= TS), which drops the separate per-warp tiles.
-template <typename T, class S, bool ALIAS = false>
+// (LS >= TS), which drops the separate per-warp tiles.  A16: rows must start
+// 16-byte aligned (bulk copies of fp32 rows).
+template <typename T, class S, bool ALIAS = false, bool A16 = false>
 constexpr int row_stride() {
   constexpr int words = (int)(sizeof(Cx<T>) / 4);
   const int base = ALIAS && TileG<T, S>::TS > S::L ? TileG<T, S>::TS : S::L;
-  int best = base, bc = phase_conflicts<S>(base, words);
-  for (int p = 1; p < 8; ++p) {
+  int best = -1, bc = 1 << 30;
+  for (int p = 0; p < 8; ++p) {
+    if (A16 && ((base + p) * (int)sizeof(Cx<T>)) % 16 != 0) continue;
     const int c = phase_conflicts<S>(base + p, words);
     if (c < bc) { bc = c; best = base + p; }
   }
   return best;
 }
+
+// forward passes: rows are staged with bulk copies whenever a row is a whole
+// number of 16-byte units (always in fp64; fp32 with even L), else per-element
+// cp.async (fp32, odd L)
+#ifndef BLR_F32_BULK
+#define BLR_F32_BULK 1
+#endif
+template <typename T, class S>
+constexpr bool fwd_bulk_rows() {
+  return sizeof(T) == 8 || (BLR_F32_BULK && (S::L * (int)sizeof(Cx<T>)) % 16 == 0);
+}
+template <typename T, class S>
+constexpr int fwd_row_stride() { return row_stride<T, S, true, sizeof(T) == 4 && fwd_bulk_rows<T, S>()>(); }
 
 template <typename T, class S>
 __global__ void __launch_bounds__(kPW * 32) k_xinv(XPassArgs<T> a, PadGeom g, const double* __restrict__ twg) {
@@ -1305,7 +1320,7 @@ template <typename T, class S>
 __global__ void __launch_bounds__(kPWF * 32, 4) k_yfwd(YFwdArgs<T> a, PadGeom g, const double* __restrict__ twg) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int LPC = kPWF * S::LPW;
-  constexpr int LS = row_stride<T, S, true>();
+  constexpr int LS = fwd_row_stride<T, S>();
   constexpr int LPCS = t_stride<LPC>();
   constexpr int SLAB = LPC * LS;
   const int P0 = g.P[0], K1 = g.K[1], B1 = g.B[1];
@@ -1316,7 +1331,7 @@ __global__ void __launch_bounds__(kPWF * 32, 4) k_yfwd(YFwdArgs<T> a, PadGeom g,
   const int per = g.Kz1 * nxb;
   const int nitems = a.nj * per;
   __shared__ uint64_t bars[2];
-  Stager<T> stg;
+  Stager<T, fwd_bulk_rows<T, S>()> stg;
   stg.init(bars);
   __syncthreads();
   auto issue = [&](int it, int t, int b) {
@@ -1489,7 +1504,7 @@ __global__ void __launch_bounds__(kPWF * 32, DEFER ? 6 : BLR_XFWD_MINB) k_xfwd(F
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int LPW = S::LPW;
   constexpr int LPC = kPWF * LPW;
-  constexpr int LS = row_stride<T, S, true>();
+  constexpr int LS = fwd_row_stride<T, S>();
   constexpr int LPCS = t_stride<LPC>();
   constexpr int SLAB = LPC * LS;
   const int K0 = g.K[0], B0 = g.B[0], B1 = g.B[1], K1 = g.K[1];
@@ -1531,7 +1546,7 @@ __global__ void __launch_bounds__(kPWF * 32, DEFER ? 6 : BLR_XFWD_MINB) k_xfwd(F
     return s - LPW + z;
   };
   __shared__ uint64_t bars[2];
-  Stager<T> stg;
+  Stager<T, fwd_bulk_rows<T, S>()> stg;
   stg.init(bars);
   __syncthreads();
   auto issue = [&](int it, int t, int b) {
@@ -1862,7 +1877,7 @@ template <typename T, class S>
 void launch_yfwd(blr_ctx* c, PadEngine* e, const YFwdArgs<T>& a) {
   const PadGeom& g = e->g;
   constexpr int LPC = kPWF * S::LPW;
-  const size_t sm = sizeof(Cx<T>) * (S::L + 2 * (size_t)LPC * row_stride<T, S, true>() +
+  const size_t sm = sizeof(Cx<T>) * (S::L + 2 * (size_t)LPC * fwd_row_stride<T, S>() +
                                      (size_t)g.B[1] * t_stride<LPC>());
   ensure_smem(k_yfwd<T, S>, sm);
   const int nxb = (g.P[0] + LPC - 1) / LPC;
@@ -1915,7 +1930,7 @@ template <typename T, class S>
 void launch_xfwd(blr_ctx* c, PadEngine* e, const FwdArgs<T>& a) {
   const PadGeom& g = e->g;
   constexpr int LPC = kPWF * S::LPW;
-  const size_t sm = sizeof(Cx<T>) * (S::L + 2 * (size_t)LPC * row_stride<T, S, true>() +
+  const size_t sm = sizeof(Cx<T>) * (S::L + 2 * (size_t)LPC * fwd_row_stride<T, S>() +
                                      (size_t)g.B[0] * t_stride<LPC>());
   const int nyb = (g.B[1] + LPC - 1) / LPC;
   const int n0 = (g.K[1] + 1 + S::LPW - 1) / S::LPW;
