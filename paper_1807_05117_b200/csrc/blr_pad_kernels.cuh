@@ -1796,8 +1796,12 @@ struct PadEngine {
 
 
 // raise the kernel's dynamic shared-memory limit once (not per launch)
+// forward-pass persistent grids: at most per_sm * nsm / BLR_FWD_GRID_DIV CTAs
+#ifndef BLR_FWD_GRID_DIV
+#define BLR_FWD_GRID_DIV 1
+#endif
 template <class K>
-static int persistent_grid(K kernel, int threads, size_t smem, int nitems) {
+static int persistent_grid(K kernel, int threads, size_t smem, int nitems, int div = 1) {
   static int per_sm = 0;  // one static per kernel instantiation (smem is fixed per instantiation)
   static int nsm = 0;
   if (!per_sm) {
@@ -1807,7 +1811,7 @@ static int persistent_grid(K kernel, int threads, size_t smem, int nitems) {
     BLR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
     if (per_sm < 1) per_sm = 1;
   }
-  return std::max(1, std::min(nitems, per_sm * nsm));
+  return std::max(1, std::min(nitems, per_sm * nsm / div));
 }
 
 template <typename K>
@@ -1881,7 +1885,7 @@ void launch_yfwd(blr_ctx* c, PadEngine* e, const YFwdArgs<T>& a) {
                                      (size_t)g.B[1] * t_stride<LPC>());
   ensure_smem(k_yfwd<T, S>, sm);
   const int nxb = (g.P[0] + LPC - 1) / LPC;
-  const int grid = persistent_grid(k_yfwd<T, S>, kPWF * 32, sm, a.nj * g.Kz1 * nxb);
+  const int grid = persistent_grid(k_yfwd<T, S>, kPWF * 32, sm, a.nj * g.Kz1 * nxb, BLR_FWD_GRID_DIV);
   launch_pdl(k_yfwd<T, S>, grid, kPWF * 32, sm, c->stream, a, g, (const double*)e->tw[1]);
   BLR_LAUNCHED();
 }
@@ -1945,7 +1949,7 @@ void launch_xfwd(blr_ctx* c, PadEngine* e, const FwdArgs<T>& a) {
     return;
   }
   ensure_smem(k_xfwd<T, S>, sm);
-  const int grid = persistent_grid(k_xfwd<T, S>, kPWF * 32, sm, items);
+  const int grid = persistent_grid(k_xfwd<T, S>, kPWF * 32, sm, items, BLR_FWD_GRID_DIV);
   launch_pdl(k_xfwd<T, S>, grid, kPWF * 32, sm, c->stream, a, g, (const double*)e->tw[0]);
   BLR_LAUNCHED();
 }
