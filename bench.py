@@ -638,6 +638,7 @@ def cpu_baseline(args, pad, reg=None, reg_hard=None):
     del ev
     with HostThreads(O, 1):
         t1, t1_sample, desc1 = cpu_stage_sample(args, pad)
+    t1_hvp = t1
     out = {"value": 1.0 / t_hvp, "unit": UNIT, "cores": cores, "kind": "port",
            "sample": f"1 whole {args.objective} GN HVP of the oracle port at {args.size}^3/K={args.band}/"
                      f"Nt={args.nt}, pad {pad[0]} (= the B200 arm's pad; the reference's own pad "
@@ -667,6 +668,15 @@ def cpu_baseline(args, pad, reg=None, reg_hard=None):
     for r, key in ((reg, "registration"), (reg_hard, "registration_hard")):
         if r and r.get("calls"):
             out[key] = estimate(r)
+    if reg and reg.get("calls"):
+        # SURVEY §8(d) "all-cores throughput for the batch": one single-threaded
+        # registration per core, each costing the all-core estimate scaled by the
+        # measured 1-core / all-core HVP ratio (an estimate built on estimates)
+        t1 = out["registration"]["cpu_s_estimate"] * (t1_hvp / t_hvp)
+        out["batch_all_cores_estimate"] = {
+            "pairs_per_s": round(cores / t1, 5), "cores": cores, "estimated": True,
+            "s_per_registration_one_core": round(t1, 1),
+            "gpu_pairs_per_s_single_registration": round(1.0 / reg["s_per_registration"], 3)}
     return out
 
 

@@ -1317,7 +1317,10 @@ struct YFwdArgs {
 // the cp.async slab of the next (item, term) load streams in while the warps
 // transform the current one, so HBM stays busy through the FFT phase.
 template <typename T, class S>
-__global__ void __launch_bounds__(kPWF * 32, 4) k_yfwd(YFwdArgs<T> a, PadGeom g, const double* __restrict__ twg) {
+#ifndef BLR_YFWD_MINB
+#define BLR_YFWD_MINB 4
+#endif
+__global__ void __launch_bounds__(kPWF * 32, BLR_YFWD_MINB) k_yfwd(YFwdArgs<T> a, PadGeom g, const double* __restrict__ twg) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int LPC = kPWF * S::LPW;
   constexpr int LS = fwd_row_stride<T, S>();
