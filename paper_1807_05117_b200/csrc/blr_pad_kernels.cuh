@@ -1400,6 +1400,69 @@ __global__ void __launch_bounds__(kPWF * 32, BLR_YFWD_MINB) k_yfwd(YFwdArgs<T> a
   }
 }
 
+// Lean one-shot forward y pass (BLR_YFWD_LEAN=1), shaped like the inverse
+// passes: one CTA per (job, kz, chunk of kPW * LPW x rows), rows staged with
+// per-element cp.async, the FFT tile overlaying each warp's own rows, the
+// job's terms summed in registers and the in-band outputs stored straight from
+// the registers to the I layout -- no shared accumulator, no persistent loop.
+#ifndef BLR_YFWD_LEAN_MINB
+#define BLR_YFWD_LEAN_MINB 0
+#endif
+template <typename T, class S>
+__global__ void __launch_bounds__(kPW * 32, BLR_YFWD_LEAN_MINB) k_yfwd_lean(YFwdArgs<T> a, PadGeom g, const double* __restrict__ twg) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int LPC = kPW * S::LPW;
+  constexpr int LS = row_stride<T, S, true>();
+  const int P0 = g.P[0], K1 = g.K[1], B1 = g.B[1];
+  T* tw = (T*)smem_raw;
+  Cx<T>* slab = (Cx<T>*)(tw + 2 * S::L);  // [LPC][LS]
+  const int nxb = (P0 + LPC - 1) / LPC;
+  const int per = g.Kz1 * nxb;
+  const int jb = blockIdx.x / per;
+  const int r = blockIdx.x - jb * per;
+  const int kz = r / nxb;
+  const int cx0 = (r - kz * nxb) * LPC;
+  const int nlc = min(LPC, P0 - cx0);
+  const int nt = a.nterms[jb];
+  const int wl0 = (threadIdx.x >> 5) * S::LPW;
+  const int nl = min(S::LPW, nlc - wl0);
+  const T kzk = (T)(kTwoPi * (double)kz);
+  load_tw_async<T>(tw, twg, S::L);
+  pdl_wait();
+  Cx<T> yacc[S::R2];
+  Cx<T>* out = a.out + jb * g.n1 + (int64_t)kz * B1 * P0 + cx0 + wl0;  // + iy * P0 + line
+  for (int t = 0; t < nt; ++t) {
+    const Cx<T>* src = a.sin[jb][t] + ((int64_t)kz * P0 + cx0) * S::L;  // nlc contiguous rows
+    for (int i = threadIdx.x; i < nlc * S::L; i += blockDim.x) {
+      const int row = i / S::L, col = i - (i / S::L) * S::L;  // compile-time divisor
+      cp_async<T>(slab + row * LS + col, src + i);
+    }
+    __pipeline_commit();
+    __pipeline_wait_prior(0);
+    __syncthreads();
+    if (nl > 0) {
+      const int ax = a.axis[jb][t];
+      const Cx<T>* sl = slab + wl0 * LS;
+      auto load = [&](int line, int y, int) -> Cx<T> { return sl[line * LS + y]; };
+      auto store = [&](int line, int q, int k2, Cx<T> v) {
+        const int iy = bin_to_index(q, S::L, K1, B1);
+        if (iy >= 0) {
+          if (ax == 1) v = mul_ik<T>(v, (T)(kTwoPi * (double)freq_of(iy, K1, B1)));
+          else if (ax == 2) v = mul_ik<T>(v, kzk);
+        }
+        yacc[k2] = t == 0 ? v : cadd(yacc[k2], v);
+        if (t == nt - 1 && iy >= 0) {
+          BLR_CHECK(jb * g.n1 + (int64_t)kz * B1 * P0 + cx0 + wl0 + line + (int64_t)iy * P0 < a.nj * g.n1,
+                    "yfwd_lean out");
+          out[(int64_t)iy * P0 + line] = yacc[k2];
+        }
+      };
+      wfft<T, S, false, true>(slab + wl0 * LS, tw, nl, load, store);
+    }
+    if (t + 1 < nt) __syncthreads();  // the slab is refilled by the next term
+  }
+}
+
 // ---------------------------------------------------------------------------
 // forward x pass + epilogue: I [..][kz][ky][x] -> band, multipliers, 1/P^3,
 // -(v + .) / negation, fused RK4 stage update (kz = 0 symmetrized in-item)
@@ -1880,9 +1943,23 @@ void launch_lines(blr_ctx* c, PadEngine* e, const LineArgs<T>& a) {
   launch_pdl(k_zlines<T, S, OP>, g.P[0] * nyc, kZWarps * 32, sm, c->stream, a, g, (const double*)e->tw[2]);
   BLR_LAUNCHED();
 }
+// A/B (r02): the lean one-shot y-forward ties the persistent one (1.77 vs 1.76
+// ms per HVP; 158 registers either way), so the persistent kernel stays
+#ifndef BLR_YFWD_LEAN
+#define BLR_YFWD_LEAN 0
+#endif
 template <typename T, class S>
 void launch_yfwd(blr_ctx* c, PadEngine* e, const YFwdArgs<T>& a) {
   const PadGeom& g = e->g;
+  if (BLR_YFWD_LEAN) {
+    constexpr int LPC = kPW * S::LPW;
+    const size_t sm = sizeof(T) * 2 * S::L + sizeof(Cx<T>) * (size_t)LPC * row_stride<T, S, true>();
+    ensure_smem(k_yfwd_lean<T, S>, sm);
+    const int nxb = (g.P[0] + LPC - 1) / LPC;
+    launch_pdl(k_yfwd_lean<T, S>, a.nj * g.Kz1 * nxb, kPW * 32, sm, c->stream, a, g, (const double*)e->tw[1]);
+    BLR_LAUNCHED();
+    return;
+  }
   constexpr int LPC = kPWF * S::LPW;
   const size_t sm = sizeof(Cx<T>) * (S::L + 2 * (size_t)LPC * fwd_row_stride<T, S>() +
                                      (size_t)g.B[1] * t_stride<LPC>());
