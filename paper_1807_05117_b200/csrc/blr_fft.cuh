@@ -531,26 +531,6 @@ __device__ __forceinline__ void wfft_b(const Cx<T>* tile, int nl, Store& store) 
   __syncwarp();
 }
 
-// step B with the outputs left in registers: u[k2] = X[k1 + R1 k2] of this
-// lane's line (line, k1 as in wfft_b); returns whether the lane holds a line.
-// Lets a caller specialize what it does with the outputs without duplicating
-// the DFT.
-template <typename T, class S, bool INV>
-__device__ __forceinline__ bool wfft_b_regs(const Cx<T>* tile, int nl, Cx<T>* u) {
-  using G = TileG<T, S>;
-  const int lane = threadIdx.x & 31;
-  const int line = lane / S::R1, k1 = lane - (lane / S::R1) * S::R1;
-  const bool act = line < nl && line < S::LPW;
-  if (act) {
-    const Cx<T>* t = tile + line * G::TS + k1 * G::KS;
-#pragma unroll
-    for (int n2 = 0; n2 < S::R2; ++n2) u[n2] = t[n2];
-    dft<T, S::R2, INV>(u);
-  }
-  __syncwarp();
-  return act;
-}
-
 template <typename T, class S, bool INV, bool ALIAS = false, class Load, class Store>
 __device__ __forceinline__ void wfft(Cx<T>* tile, const T* twr, int nl, Load load, Store store) {
   wfft_a<T, S, INV, ALIAS>(tile, twr, nl, load);

@@ -37,7 +37,7 @@ BLR_FOR_EACH_LZ(BLR_EXTERN_F2)
 #define BLR_EXTERN_L_ALLOPS(LL, A, B) \
   BLR_EXTERN_LZ(LL, A, B, 0) BLR_EXTERN_LZ(LL, A, B, 1) BLR_EXTERN_LZ(LL, A, B, 2) BLR_EXTERN_LZ(LL, A, B, 3) \
   BLR_EXTERN_LZ(LL, A, B, 4) BLR_EXTERN_LZ(LL, A, B, 5) BLR_EXTERN_LZ(LL, A, B, 6) BLR_EXTERN_LZ(LL, A, B, 7) \
-  BLR_EXTERN_LZ(LL, A, B, 8) BLR_EXTERN_LZ(LL, A, B, 9)
+  BLR_EXTERN_LZ(LL, A, B, 8)
 BLR_FOR_EACH_LZ(BLR_EXTERN_L_ALLOPS)
 #undef BLR_EXTERN_L_ALLOPS
 #undef BLR_EXTERN_LZ
@@ -64,12 +64,6 @@ void pad_engine_release(blr_ctx* c) {
     if (p) cudaFree(p);
   for (auto* p : it->second.buf)
     if (p) cudaFree(p);
-  PadEngine& e = it->second;
-  if (e.aux) {
-    cudaStreamSynchronize(e.aux);
-    cudaStreamDestroy(e.aux);
-    for (cudaEvent_t ev : {e.ev_start, e.ev_q[0], e.ev_q[1], e.ev_used[0], e.ev_used[1]}) cudaEventDestroy(ev);
-  }
   engines().erase(it);
 }
 
@@ -272,7 +266,7 @@ static void acc_tables(int op, LineArgs<T>& a) {
   const int d = a.d, dd = d * d;
   for (int f = 0; f < kMaxLineS; ++f) { a.oi[f] = 0; a.ri[f] = 0; a.sg[f] = 1.0; }
   a.nst = 0;
-  if (op == kOpMap || op == kOpMapTC || op == kOpMapTQ) {
+  if (op == kOpMap || op == kOpMapTC) {
     // staged slots: V_j
     a.nst = d;
     for (int j = 0; j < d; ++j) a.st_idx[j] = (op == kOpMapTC ? dd : 0) + j;
@@ -292,8 +286,7 @@ static void acc_tables(int op, LineArgs<T>& a) {
 
 static const char* const kLineOpName[] = {"pad_zlines_realize", "pad_zlines_map",     "pad_zlines_map_tc",
                                           "pad_zlines_map_tf",  "pad_zlines_inv_vol", "pad_zlines_bwd_vol",
-                                          "pad_zlines_outer",   "pad_zlines_outer_pair", "pad_zlines_contract",
-                                          "pad_zlines_map_tq"};
+                                          "pad_zlines_outer",   "pad_zlines_outer_pair", "pad_zlines_contract"};
 
 template <typename T, int OP>
 static void lines(blr_ctx* c, PadEngine* e, LineArgs<T>& a, double bytes) {
@@ -451,13 +444,6 @@ static void fwd2d(blr_ctx* c, PadEngine* e, const std::vector<FwdSpec<T>>& outs,
     a.cur = rk.cur ? (Cx<T>*)rk.cur + shift : nullptr;
     a.acc = rk.acc ? (Cx<T>*)rk.acc + shift : nullptr;
     a.stage = rk.stage ? (Cx<T>*)rk.stage + shift : nullptr;
-// BLR_XFWD_DEFER=1: the x pass writes its results and k_xfwd_epi applies the
-// epilogue (156 instead of 226 registers in the transform kernel).  A/B (r02):
-// x-forward 1.92 -> 2.04 ms per HVP, so off.
-#ifndef BLR_XFWD_DEFER
-#define BLR_XFWD_DEFER 0
-#endif
-    a.kres = BLR_XFWD_DEFER ? (Cx<T>*)e_scratch(c, e, 2, (size_t)a.no * g.nh * sizeof(Cx<T>)) : nullptr;
     {
       ProfScope ps(c, "pad_xpass_fwd", ((double)nterm * g.n1 + a.no * g.nh * (rk.s ? 4 : 2)) * sizeof(Cx<T>));
       dispatch_xfwd<T>(c, e, a);
@@ -752,38 +738,6 @@ bool inverse_map_and_volume_v2(blr_ctx* c, FlowRef v, int substeps, Cx<T>* psi, 
   return true;
 }
 
-// q_o = sum_j Du_oj dV_j on the pad grid (the D(u) . dv term of the cached
-// tangent RHS, transport.py:216-228), for one RK4 stage.  A streaming kernel on
-// the engine's side stream: it reads 9 + 3 and writes 3 real pad fields while
-// the main stream runs the stage's inverse x / y passes (latency-bound, HBM
-// mostly idle), so the z-line kernel (kOpMapTQ) reads 3 fields instead of 12.
-template <typename T>
-__global__ void __launch_bounds__(256) k_dudv(const T* __restrict__ du, const T* __restrict__ dv, int d,
-                                              int64_t np, T* __restrict__ q) {
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < np; p += (int64_t)gridDim.x * blockDim.x) {
-    T dvj[3];
-#pragma unroll
-    for (int j = 0; j < 3; ++j) dvj[j] = j < d ? dv[j * np + p] : (T)0;
-#pragma unroll
-    for (int o = 0; o < 3; ++o) {
-      if (o >= d) continue;
-      T s = 0;
-#pragma unroll
-      for (int j = 0; j < 3; ++j)
-        if (j < d) s += du[(o * d + j) * np + p] * dvj[j];
-      q[o * np + p] = s;
-    }
-  }
-}
-
-static int g_tq_disabled = -1;
-
-static void ensure_aux(PadEngine* e) {
-  if (e->aux) return;
-  BLR_CUDA(cudaStreamCreateWithFlags(&e->aux, cudaStreamNonBlocking));
-  for (cudaEvent_t* ev : {&e->ev_start, &e->ev_q[0], &e->ev_q[1], &e->ev_used[0], &e->ev_used[1]})
-    BLR_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
-}
 
 template <typename T>
 bool state_tangents_v2(blr_ctx* c, FlowRef v, FlowRef dv, int substeps, int flags, const T* du_cache,
@@ -807,40 +761,10 @@ bool state_tangents_v2(blr_ctx* c, FlowRef v, FlowRef dv, int substeps, int flag
     Cx<T>* S = tmp.get<Cx<T>>(nsi * pg.ns);
     Cx<T>* So = tmp.get<Cx<T>>(2 * d * pg.ns);
     const int du0 = cached ? 0 : d;
-    // Opt-in (BLR_MAPTQ=1): with the D(u) cache and a stationary dv, compute
-    // Du . dV per stage on the side stream (k_dudv, double-buffered q) and let
-    // the kOpMapTQ z-lines read 3 real fields instead of 12.  A/B on the B200
-    // (r02): map_tq 2.54 vs map_tc 2.81 ms per HVP, but k_dudv (1.45 ms) does
-    // not overlap the pass kernels (their CTAs hold the SMs; xfwd slows down),
-    // deformation GN HVP 10.47 vs 9.78 ms -- so the single-kernel MapTC stays.
-    if (g_tq_disabled < 0) {
-      const char* env = getenv("BLR_MAPTQ");
-      g_tq_disabled = (env && env[0] == '1') ? 0 : 1;
-    }
-    const bool tq = cached && dv.stationary() && !g_tq_disabled;
-    T* qbuf = nullptr;
-    if (tq) {
-      ensure_aux(e);
-      qbuf = tmp.get<T>(2 * (int64_t)d * pg.np);
-      BLR_CUDA(cudaEventRecord(e->ev_start, c->stream));  // dV realized, Du cache written
-      BLR_CUDA(cudaStreamWaitEvent(e->aux, e->ev_start, 0));
-    }
     rk4_v2<T>(c, e, v.n_steps, substeps, true, cur, ncomp, {{du0, d, dphi, (flags & 8) != 0}}, tmp,
               [&](int si, double t, const Cx<T>* s, const Rk& rk) {
                 const auto& vt = V.at(t);
                 const auto& dvt = dV.at(t);
-                const int qb = si & 1;
-                T* q = tq ? qbuf + (int64_t)qb * d * pg.np : nullptr;
-                if (tq) {
-                  if (si >= 2) BLR_CUDA(cudaStreamWaitEvent(e->aux, e->ev_used[qb], 0));
-                  {
-                    ProfScope ps(c, "pad_dudv", (double)(d * d + 2 * d) * pg.np * sizeof(T), e->aux);
-                    k_dudv<T><<<grid_blocks(pg.np, 256, 148 * 8), 256, 0, e->aux>>>(
-                        du_cache + (int64_t)si * dd * pg.np, dvt.real, d, pg.np, q);
-                    BLR_LAUNCHED();
-                  }
-                  BLR_CUDA(cudaEventRecord(e->ev_q[qb], e->aux));
-                }
                 std::vector<InvSpec<T>> f;
                 push_jac<T>(g, pg, s, f);
                 if (!cached) push_jac<T>(g, pg, s + d * pg.nh, f);
@@ -850,19 +774,7 @@ bool state_tangents_v2(blr_ctx* c, FlowRef v, FlowRef dv, int substeps, int flag
                 la.d = d;
                 for (int i = 0; i < nsi; ++i) la.sin[i] = S + i * pg.ns;
                 std::vector<FwdSpec<T>> outs;
-                if (tq) {
-                  la.ns = dd; la.nr = 2 * d; la.no = d;
-                  for (int j = 0; j < d; ++j) {
-                    la.rin[j] = vt.real + j * pg.np;
-                    la.rin[d + j] = q + j * pg.np;
-                  }
-                  for (int i = 0; i < d; ++i) la.sout[i] = So + i * pg.ns;
-                  BLR_CUDA(cudaStreamWaitEvent(c->stream, e->ev_q[qb], 0));
-                  lines<T, kOpMapTQ>(c, e, la, sbytes(pg, dd, 2 * d, d, 0, sizeof(T)));
-                  BLR_CUDA(cudaEventRecord(e->ev_used[qb], c->stream));
-                  for (int i = 0; i < d; ++i)
-                    outs.push_back(fwd1<T>(So + i * pg.ns, kEpiNegAdd, dvt.H + i * pg.nh));
-                } else if (cached) {
+                if (cached) {
                   la.ns = dd; la.nr = dd + 2 * d; la.no = d;
                   const T* Du = du_cache + (int64_t)si * dd * pg.np;
                   for (int i = 0; i < dd; ++i) la.rin[i] = Du + i * pg.np;

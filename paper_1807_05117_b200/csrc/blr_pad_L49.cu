@@ -16,7 +16,6 @@ template void launch_lines<double, WShape<7, 7>, 5>(blr_ctx*, PadEngine*, const 
 template void launch_lines<double, WShape<7, 7>, 6>(blr_ctx*, PadEngine*, const LineArgs<double>&);
 template void launch_lines<double, WShape<7, 7>, 7>(blr_ctx*, PadEngine*, const LineArgs<double>&);
 template void launch_lines<double, WShape<7, 7>, 8>(blr_ctx*, PadEngine*, const LineArgs<double>&);
-template void launch_lines<double, WShape<7, 7>, 9>(blr_ctx*, PadEngine*, const LineArgs<double>&);
 template void launch_xinv<float, WShape<7, 7>>(blr_ctx*, PadEngine*, const XPassArgs<float>&);
 template void launch_yinv<float, WShape<7, 7>>(blr_ctx*, PadEngine*, const YPassArgs<float>&);
 template void launch_yfwd<float, WShape<7, 7>>(blr_ctx*, PadEngine*, const YFwdArgs<float>&);
@@ -30,7 +29,6 @@ template void launch_lines<float, WShape<7, 7>, 5>(blr_ctx*, PadEngine*, const L
 template void launch_lines<float, WShape<7, 7>, 6>(blr_ctx*, PadEngine*, const LineArgs<float>&);
 template void launch_lines<float, WShape<7, 7>, 7>(blr_ctx*, PadEngine*, const LineArgs<float>&);
 template void launch_lines<float, WShape<7, 7>, 8>(blr_ctx*, PadEngine*, const LineArgs<float>&);
-template void launch_lines<float, WShape<7, 7>, 9>(blr_ctx*, PadEngine*, const LineArgs<float>&);
 template void launch_fwd2<double, WShape<7, 7>>(blr_ctx*, PadEngine*, const Fwd2Args<double>&, int, int);
 template bool fwd2_fits<double, WShape<7, 7>>(const PadGeom&);
 template void launch_fwd2<float, WShape<7, 7>>(blr_ctx*, PadEngine*, const Fwd2Args<float>&, int, int);

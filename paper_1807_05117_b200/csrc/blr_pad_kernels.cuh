@@ -79,29 +79,6 @@ __device__ __forceinline__ bool load_tw_async(T* dst, const double* src, int L) 
 template <typename T>
 __device__ __forceinline__ Cx<T> mul_ik(Cx<T> z, T k) { return cx<T>(-(k * z.y), k * z.x); }
 
-// Per-lane step-A gather table of an inverse pass: lane (line, n2) reads grid
-// bin q = R2 n1 + n2 for n1 = 0..R1-1; off[n1] = band index * stride (or -1
-// outside the band), kk[n1] = 2 pi k of that band index.  Built once per CTA
-// instead of per element (bin_to_index / freq_of / int->fp64 per gathered value).
-// A/B (r02): neutral (y-inverse 1.47 vs 1.45 ms), so off.
-#ifndef BLR_PASS_TABLES
-#define BLR_PASS_TABLES 0
-#endif
-template <typename T, class S>
-struct GatherTab {
-  int off[S::R1];
-  T kk[S::R1];
-  __device__ __forceinline__ void build(int K, int B, int stride) {
-    const int n2 = (threadIdx.x & 31) % S::R2;
-#pragma unroll
-    for (int n1 = 0; n1 < S::R1; ++n1) {
-      const int b = bin_to_index(S::R2 * n1 + n2, S::L, K, B);
-      off[n1] = b >= 0 ? b * stride : -1;
-      kk[n1] = (T)(kTwoPi * (double)freq_of(b >= 0 ? b : 0, K, B));
-    }
-  }
-};
-
 // ---------------------------------------------------------------------------
 // inverse x pass: band H [kz][kx][ky] -> I [xf][kz][ky][x]
 // ---------------------------------------------------------------------------
@@ -336,17 +313,9 @@ __global__ void __launch_bounds__(kPW * 32) k_xinv(XPassArgs<T> a, PadGeom g, co
     BLR_CHECK(((int64_t)kz * B1 + cky0 + wl0 + line) * S::L + x < g.n1, "xinv out");
     out[line * S::L + x] = v;
   };
-  if (BLR_PASS_TABLES) {
-    GatherTab<T, S> tb;
-    tb.build(K0, B0, LPCS);
-    auto load = [&](int line, int, int n1) -> Cx<T> {
-      const int o = tb.off[n1];
-      Cx<T> z = sl[(o >= 0 ? o : 0) + line];
-      if (mulx) z = mul_ik<T>(z, tb.kk[n1]);
-      return o >= 0 ? z : cx<T>(0, 0);
-    };
-    wfft<T, S, true>(tile, tw, nl, load, store);
-  } else if (mulx) {  // uniform per CTA: two gathers instead of a per-element branch
+  // (a per-lane gather table of band offsets / wavenumbers built once per CTA
+  // measured neutral, A/B r02)
+  if (mulx) {  // uniform per CTA: two gathers instead of a per-element branch
     auto load = [&](int line, int p, int) -> Cx<T> {
       const int ix = bin_to_index(p, S::L, K0, B0);
       const int ixc = ix >= 0 ? ix : 0;
@@ -434,37 +403,7 @@ __global__ void __launch_bounds__(kPW * 32) k_yinv(YPassArgs<T> a, PadGeom g, co
     BLR_CHECK(((int64_t)kz * P0 + cx0 + wl0 + line) * S::L + y < g.ns, "yinv out");
     out[line * S::L + y] = v;
   };
-  if (BLR_PASS_TABLES) {
-    GatherTab<T, S> tb;
-    tb.build(K1, B1, LPCS);
-    if (nt == 1) {
-      const int ax0 = ax[0];
-      const T m0 = ax0 == 2 ? kzk : (T)0;
-      const Cx<T>* sl = slab + wl0;
-      auto load1 = [&](int line, int, int n1) -> Cx<T> {
-        const int o = tb.off[n1];
-        Cx<T> z = sl[(o >= 0 ? o : 0) + line];
-        if (ax0 >= 1) z = mul_ik<T>(z, ax0 == 1 ? tb.kk[n1] : m0);
-        return o >= 0 ? z : cx<T>(0, 0);
-      };
-      wfft<T, S, true>(tile, tw, nl, load1, store);
-    } else {
-      auto loadn = [&](int line, int, int n1) -> Cx<T> {
-        const int o = tb.off[n1];
-        const int oc = o >= 0 ? o : 0;
-        Cx<T> acc = cx<T>(0, 0);
-#pragma unroll
-        for (int t = 0; t < 3; ++t) {
-          if (ax[t] < -1) break;
-          Cx<T> z = slab[t * B1 * LPCS + oc + wl0 + line];
-          if (ax[t] >= 1) z = mul_ik<T>(z, ax[t] == 1 ? tb.kk[n1] : kzk);
-          acc = cadd(acc, z);
-        }
-        return o >= 0 ? acc : cx<T>(0, 0);
-      };
-      wfft<T, S, true>(tile, tw, nl, loadn, store);
-    }
-  } else if (nt == 1) {
+  if (nt == 1) {
     // single-term output (the common case): no term loop in the gather
     const int ax0 = ax[0];
     const Cx<T>* sl = slab + wl0;
@@ -495,7 +434,6 @@ enum LineOp {
   kOpOuter = 6,     // out_ij = rho_i V_j
   kOpOuterPair = 7, // out = [rho x V | drho x V + rho x dV]
   kOpContract = 8,  // out_i = sum_n w_n sum_j M_n(ji|ij) rho_n,j   (M real, cached)
-  kOpMapTQ = 9,     // out_i = sum_j S[ij] V_j + q_i   (q = Du . dV precomputed by k_dudv, real)
 };
 
 constexpr int kMaxLineS = 28;
@@ -530,26 +468,22 @@ struct LineArgs {
 //   REAL ops: realized inputs are kept in shared memory and the outputs are
 //            formed on the fly while loading the R2C.
 template <int OP> struct ZOp {
-  static constexpr bool acc = OP == kOpMap || OP == kOpMapTC || OP == kOpInvVol || OP == kOpContract ||
-                              OP == kOpMapTQ;
+  static constexpr bool acc = OP == kOpMap || OP == kOpMapTC || OP == kOpInvVol || OP == kOpContract;
   static constexpr int nomax = OP == kOpInvVol ? 4 : 3;
 };
 
 constexpr int kZWarps = 2;
 // Occupancy targets (CTAs per SM) of the z-line kernel per op; 0 = registers
 // unconstrained.  The outer op is held at 6 CTAs per SM (its shared-memory
-// limit; see BLR_ZUNROLL_OUTER).
+// limit with the unrolled outer products).
 #ifndef BLR_ZMINB_OUTER
 #define BLR_ZMINB_OUTER 6
 #endif
 #ifndef BLR_ZMINB_MAPTC
 #define BLR_ZMINB_MAPTC 0
 #endif
-#ifndef BLR_ZMINB_MAPTQ
-#define BLR_ZMINB_MAPTQ 0
-#endif
 constexpr int zline_min_blocks(int op) {
-  return op == 6 ? BLR_ZMINB_OUTER : op == 2 ? BLR_ZMINB_MAPTC : op == 9 ? BLR_ZMINB_MAPTQ : 0;
+  return op == 6 ? BLR_ZMINB_OUTER : op == 2 ? BLR_ZMINB_MAPTC : 0;
 }
 
 // z-line shared buffers, line strides chosen by the bank model (blr_fft.cuh):
@@ -666,18 +600,14 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
   const int nreal = OP == kOpContract ? a.d : (Tr::acc || OP == kOpRealize) ? 0 : ns_blk;
   // shared layout: tw | per warp { tile | stage[max(2*2*Kz1*LPW, LPW*L)] (xbuf aliases it after the
   //                                 C2R phase) | Vst[nst][LPW*L] | Rsm[nreal][LPW*L] }
-  // BLR_ZROW=1: each field's stage region ends with its own zero row, so the
-  // Hermitian gather indexes out-of-band rows with the in-band arithmetic (no
-  // select); A/B (r02): the outer op loses a CTA per SM to the extra rows
-  // (2.14 -> 2.31 ms), so the default keeps one shared zero row after them
-#ifndef BLR_ZROW
-#define BLR_ZROW 0
-#endif
-  const int fstride = (Kz1 + BLR_ZROW) * S::LPW;  // per-field stage: Kz1 spectra rows (+ zero row)
-  const int zoff = 4 * fstride;                   // shared zero row (BLR_ZROW=0) / end of regions
+  // (one shared zero row after the four field regions serves the out-of-band
+  // rows of the Hermitian gather; per-field zero rows cost the outer op a CTA
+  // per SM, A/B r02 2.14 -> 2.31 ms)
+  const int fstride = Kz1 * S::LPW;  // per-field stage: Kz1 spectra rows
+  const int zoff = 4 * fstride;      // the shared zero row
   using ZG = ZLineG<T, S>;
   constexpr int LX = ZG::LX, LR = ZG::LR;
-  const int stage_n = max(zoff + (BLR_ZROW ? 0 : S::LPW), S::LPW * LX);  // must match launch_lines
+  const int stage_n = max(zoff + S::LPW, S::LPW * LX);  // must match launch_lines
   const int nst = Tr::acc ? a.nst : 0;
   const size_t warp_bytes = sizeof(Cx<T>) * ((size_t)TileG<T, S>::TILE + stage_n) +
                             sizeof(T) * (size_t)(nreal + nst) * S::LPW * LR;
@@ -749,7 +679,7 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
 #pragma unroll
     for (int n1 = 0; n1 < S::R1; ++n1) {
       const int k = S::R2 * n1 + n2;
-      int row = BLR_ZROW ? Kz1 : -1, sgn = 1;  // out of band: a zero row
+      int row = -1, sgn = 1;  // out of band: the zero row
       if (k == 0) { row = 0; sgn = 0; }
       else if (k <= K2) { row = k; sgn = 1; }
       else if (k >= L - K2) { row = L - k; sgn = -1; }
@@ -758,11 +688,7 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
     }
   }
   // the shared zero row (never overwritten by the prefetch)
-  if (BLR_ZROW) {
-    if (lane < 4 * S::LPW) stage[(lane / S::LPW) * fstride + Kz1 * S::LPW + lane % S::LPW] = cx<T>(0, 0);
-  } else if (lane < S::LPW) {
-    stage[zoff + lane] = cx<T>(0, 0);
-  }
+  if (lane < S::LPW) stage[zoff + lane] = cx<T>(0, 0);
   const int npair = (ns_blk + 1) / 2;
   const int nloop = OP == kOpContract ? a.n_nodes : 1;
   const int total = nloop * npair;
@@ -770,11 +696,8 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
   // per-lane element offsets of the spectra gather, fixed across fields and
   // pairs: slot j covers stage entry i = lane + 32 j -> (row k, line l), global
   // offset k * kzs + l (32-bit: Kz1 * P0 * P1 < 2^31); -1 marks an empty slot
-#ifndef BLR_PF_OFFS
-#define BLR_PF_OFFS 1
-#endif
   // Kz1 = K + 1 <= (L - 1) / 3 + 1 since the pad satisfies L >= 3K + 1
-  constexpr int kPfSlots = BLR_PF_OFFS ? (S::LPW * ((S::L - 1) / 3 + 1) + 31) / 32 : 1;
+  constexpr int kPfSlots = (S::LPW * ((S::L - 1) / 3 + 1) + 31) / 32;
   int pf_off[kPfSlots];
 #pragma unroll
   for (int j = 0; j < kPfSlots; ++j) {
@@ -793,19 +716,12 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
         break;
       }
       const Cx<T>* src = a.sin[f] + noff + sline;
-#if BLR_PF_OFFS
 #pragma unroll
       for (int j = 0; j < kPfSlots; ++j) {
         if (pf_off[j] >= 0) __pipeline_memcpy_async(st + ff * fstride + lane + 32 * j, src + pf_off[j], sizeof(Cx<T>));
         BLR_CHECK(pf_off[j] < 0 || ((q & 1) * 2 * fstride + ff * fstride + lane + 32 * j < zoff &&
                                     sline + pf_off[j] < g.ns), "zlines sin");
       }
-#else
-      for (int i = lane; i < Kz1 * S::LPW; i += 32) {
-        const int k = i / S::LPW, l = i - (i / S::LPW) * S::LPW;  // compile-time divisor
-        if (l < nl) __pipeline_memcpy_async(st + ff * fstride + i, src + k * kzs + l, sizeof(Cx<T>));
-      }
-#endif
     }
     __pipeline_commit();
   };
@@ -827,40 +743,17 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
   // loads are issued before that pair's transform and consumed after it, so
   // the D(u) / dv reads overlap FFT work instead of stalling the kernel start.
   // Absent components (d < 3) read component 0 and are masked.
-// Rotating accumulators (BLR_ZROT=1): A/B (r02) map_tc 2.70 -> 3.12 ms (the
-// rotations' register moves and a longer live range), so off
-#ifndef BLR_ZROT
-#define BLR_ZROT 0
-#endif
-  constexpr bool kRotOp = BLR_ZROT && (OP == kOpMap || OP == kOpMapTC);
-  const bool rot = kRotOp && a.d == 3 && ns_blk == 9;
-  const bool sw3 = (OP == kOpMap || OP == kOpMapTC) && a.d == 3 && ns_blk == 9 && total == 5;
-  // MapTQ: the same chunked schedule for acc_i += q_i, q = Du . dV precomputed
-  // (rin: V [0,d) q [d,2d)): 3 loads per position instead of 12.
   constexpr int DCH = (S::R2 + 4) / 5;  // k2 columns per chunk
-  constexpr bool kDu = OP == kOpMapTC || OP == kOpMapTQ;
-  T dbuf[kDu ? DCH : 1][OP == kOpMapTQ ? 3 : 12];
+  constexpr bool kDu = OP == kOpMapTC;
+  T dbuf[kDu ? DCH : 1][12];
   auto du_issue = [&](auto cc) {
     constexpr int c = decltype(cc)::value;
-    if constexpr (OP == kOpMapTQ) {
-      const int d = a.d;
-      const int64_t base = rline + (own ? bl : 0) * L + k1;
-      BLR_CHECK(base + S::R1 * (S::R2 - 1) < g.np, "zlines q");
-#pragma unroll
-      for (int u = 0; u < DCH; ++u) {
-        const int k2 = c * DCH + u;
-        if (k2 >= S::R2) continue;
-#pragma unroll
-        for (int o = 0; o < 3; ++o) dbuf[u][o] = __ldg(a.rin[d + (o < d ? o : 0)] + base + S::R1 * k2);
-      }
-    } else if constexpr (OP == kOpMapTC) {
+    if constexpr (OP == kOpMapTC) {
       const int d = a.d, dd = d * d;
       const int64_t base = rline + (own ? bl : 0) * L + k1;
       BLR_CHECK(base + S::R1 * (S::R2 - 1) < g.np, "zlines du");
 #pragma unroll
       for (int u = 0; u < DCH; ++u) {
-        constexpr int dummy = 0;
-        (void)dummy;
         const int k2 = c * DCH + u;
         if (k2 >= S::R2) continue;
 #pragma unroll
@@ -878,18 +771,7 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
   };
   auto du_acc = [&](auto cc) {
     constexpr int c = decltype(cc)::value;
-    // rotations done before pair c (3-D Map / MapTC order: after pairs 1, 2, 4)
-    constexpr int RC = c >= 3 ? 2 : (c >= 2 ? 1 : 0);
-    if constexpr (OP == kOpMapTQ) {
-      const int d = a.d;
-#pragma unroll
-      for (int u = 0; u < DCH; ++u) {
-        const int k2 = c * DCH + u;
-        if (k2 >= S::R2) continue;
-#pragma unroll
-        for (int o = 0; o < NOM; ++o) acc[o][k2] += (o < d && o < 3) ? dbuf[u][o < 3 ? o : 0] : (T)0;
-      }
-    } else if constexpr (OP == kOpMapTC) {
+    if constexpr (OP == kOpMapTC) {
       const int d = a.d;
 #pragma unroll
       for (int u = 0; u < DCH; ++u) {
@@ -900,12 +782,6 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
           T sdu = 0;
 #pragma unroll
           for (int j = 0; j < 3; ++j) sdu += (j < d ? dbuf[u][3 + 3 * (o < 3 ? o : 0) + j] : (T)0) * dbuf[u][j];
-          if constexpr (kRotOp && NOM == 3) {
-            if (rot) {
-              acc[(o - RC + 3) % 3][k2] += sdu;
-              continue;
-            }
-          }
           acc[o][k2] += sdu;
         }
       }
@@ -921,12 +797,8 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
       default: break;
     }
   };
-  // One input pair.  QS >= 0: the pair index is a compile-time constant (3-D
-  // Map / MapTC, all five pairs unrolled), so each realized field adds to its
-  // one output accumulator with a single FMA (output / V slot / sign known at
-  // compile time) instead of a multiply-add into every output.
-  auto pair_step = [&](int q, auto qc) {
-    constexpr int QS = decltype(qc)::value;
+  // one input pair
+  auto pair_step = [&](int q) {
     if (q + 1 < total) {
       prefetch(q + 1);
       __pipeline_wait_prior(1);
@@ -942,11 +814,7 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
     T c1[NOM], c2[NOM];
     const T* V1 = Vst;
     const T* V2 = Vst;
-    // rotating accumulators (3-D Map / MapTC): the output being filled always
-    // sits in acc[0]; a pair adds to acc[0] (and, when it straddles two
-    // outputs, acc[1]) -- 2 FMAs per realized value instead of 6
-    const bool split = rot && (f + 1) / 3 != f / 3 && two;
-    if constexpr (Tr::acc && OP != kOpContract && QS < 0) {
+    if constexpr (Tr::acc && OP != kOpContract) {
       const int o1 = a.oi[f], o2 = two ? a.oi[f + 1] : -1;
       const T sg1 = (T)a.sg[f], sg2 = two ? (T)a.sg[f + 1] : (T)0;
 #pragma unroll
@@ -961,8 +829,8 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
       // branch-free Hermitian packing of F1 + i F2 (zero rows index the zero pad row)
       const int h = hidx[n1];
       BLR_CHECK((h >= 0 ? st2o + h : zoff) + line < stage_n, "zlines gather");
-      const Cx<T> F1 = stage[(BLR_ZROW || h >= 0 ? st1o + h : zoff) + line];
-      const Cx<T> F2 = stage[(BLR_ZROW || h >= 0 ? st2o + h : zoff) + line];
+      const Cx<T> F1 = stage[(h >= 0 ? st1o + h : zoff) + line];
+      const Cx<T> F2 = stage[(h >= 0 ? st2o + h : zoff) + line];
       const T sg = (T)hsg[n1];
       return cx<T>(F1.x - sg * F2.y, sg * F1.y + F2.x);
     };
@@ -977,15 +845,6 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
       } else if constexpr (!Tr::acc || OP == kOpContract) {
         Rsm[f * ldR + li] = v.x;
         if (two) Rsm[(f + 1) * ldR + li] = v.y;
-      } else if constexpr (QS >= 0) {
-        // 3-D Map / MapTC: field F = (i, j) = (F / 3, F % 3) adds S_ij V_j to output i
-        constexpr int F1 = 2 * QS, F2 = 2 * QS + 1;
-        if (OP == kOpMap && a.wout[F1]) {
-          a.wout[F1][gi] = v.x;
-          if (F2 < 9) a.wout[F2][gi] = v.y;
-        }
-        acc[F1 / 3][k2] += v.x * Vst[(F1 % 3) * ldR + li];
-        if constexpr (F2 < 9) acc[F2 / 3][k2] += v.y * Vst[(F2 % 3) * ldR + li];
       } else {
         if (OP == kOpMap && a.wout[f]) {
           a.wout[f][gi] = v.x;
@@ -993,77 +852,13 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
         }
         const T p1 = v.x * V1[li];
         const T p2 = v.y * V2[li];
-        if constexpr (kRotOp) {
-          if (rot) {
-            acc[0][k2] += p1 + (split ? (T)0 : p2);
-            acc[1][k2] += split ? p2 : (T)0;
-            return;
-          }
-        }
 #pragma unroll
         for (int o = 0; o < NOM; ++o) acc[o][k2] += c1[o] * p1 + c2[o] * p2;
       }
     };
-    if constexpr (kDu) {
-      if constexpr (QS >= 0) du_issue(std::integral_constant<int, QS>{});
-      else du_chunk(q, du_issue);
-    }
-// A/B (r02): neutral (9.17 vs 9.14 ms), so off
-#ifndef BLR_ZPAIRSW
-#define BLR_ZPAIRSW 0
-#endif
-    if constexpr (BLR_ZPAIRSW && (OP == kOpMap || OP == kOpMapTC) && QS < 0) {
-      if (sw3) {
-        // 3-D Map / MapTC: the DFT outputs stay in registers and a warp-uniform
-        // switch on the pair applies compile-time output / V slots (one FMA per
-        // realized value; the DFT is not duplicated)
-        wfft_a<T, S, true>(tile, twp, nl, load);
-        Cx<T> u[S::R2];
-        if (wfft_b_regs<T, S, true>(tile, nl, u)) {
-          auto apply = [&](auto pc) {
-            constexpr int PC = decltype(pc)::value;
-            constexpr int F1 = 2 * PC, F2 = 2 * PC + 1;
-#pragma unroll
-            for (int k2 = 0; k2 < S::R2; ++k2) {
-              const int li = bl * LR + k1 + S::R1 * k2;
-              if (OP == kOpMap && a.wout[F1]) {
-                const int64_t gi = rline + bl * L + k1 + S::R1 * k2;
-                a.wout[F1][gi] = u[k2].x;
-                if (F2 < 9) a.wout[F2][gi] = u[k2].y;
-              }
-              acc[F1 / 3][k2] += u[k2].x * Vst[(F1 % 3) * ldR + li];
-              if constexpr (F2 < 9) acc[F2 / 3][k2] += u[k2].y * Vst[(F2 % 3) * ldR + li];
-            }
-          };
-          switch (p) {
-            case 0: apply(std::integral_constant<int, 0>{}); break;
-            case 1: apply(std::integral_constant<int, 1>{}); break;
-            case 2: apply(std::integral_constant<int, 2>{}); break;
-            case 3: apply(std::integral_constant<int, 3>{}); break;
-            default: apply(std::integral_constant<int, 4>{}); break;
-          }
-        }
-      } else {
-        wfft<T, S, true>(tile, twp, nl, load, store);
-      }
-    } else {
-      wfft<T, S, true>(tile, twp, nl, load, store);
-    }
-    if constexpr (kDu) {
-      if constexpr (QS >= 0) du_acc(std::integral_constant<int, QS>{});
-      else du_chunk(q, du_acc);
-    }
-    if constexpr (kRotOp && NOM == 3) {
-      if (rot && (f % 3 == 2 || (two && (f + 1) % 3 == 2))) {  // an output completed: rotate
-#pragma unroll
-        for (int k2 = 0; k2 < S::R2; ++k2) {
-          const T t0 = acc[0][k2];
-          acc[0][k2] = acc[1][k2];
-          acc[1][k2] = acc[2][k2];
-          acc[2][k2] = t0;
-        }
-      }
-    }
+    if constexpr (kDu) du_chunk(q, du_issue);
+    wfft<T, S, true>(tile, twp, nl, load, store);
+    if constexpr (kDu) du_chunk(q, du_acc);
     if constexpr (OP == kOpContract) {
       if (p == npair - 1) {
         // node complete: rho_n is realized in Rsm.  Stream the cached D(phi_n)
@@ -1110,23 +905,9 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
       }
     }
   };
-  // A/B on the B200: unrolling the five MapTC pairs made map_tc 37% slower
-  // (2.82 -> 3.86 ms per HVP: code size and spills), so it is off by default.
-#ifndef BLR_ZUNROLL_PAIRS
-#define BLR_ZUNROLL_PAIRS 0
-#endif
-  constexpr bool kUnrollPairs = BLR_ZUNROLL_PAIRS != 0 && (OP == kOpMap || OP == kOpMapTC);
-  if (kUnrollPairs && a.d == 3 && total == 5) {
-    if constexpr (kUnrollPairs) {
-      pair_step(0, std::integral_constant<int, 0>{});
-      pair_step(1, std::integral_constant<int, 1>{});
-      pair_step(2, std::integral_constant<int, 2>{});
-      pair_step(3, std::integral_constant<int, 3>{});
-      pair_step(4, std::integral_constant<int, 4>{});
-    }
-  } else {
-    for (int q = 0; q < total; ++q) pair_step(q, std::integral_constant<int, -1>{});
-  }
+  // (unrolling the five 3-D MapTC pairs with compile-time output slots: A/B
+  // r02 map_tc 2.82 -> 3.86 ms, code size and spills)
+  for (int q = 0; q < total; ++q) pair_step(q);
   if constexpr (kDu) {
     for (int c = total; c < 5; ++c) {  // fewer than five input pairs (d < 3)
       du_chunk(c, du_issue);
@@ -1135,32 +916,11 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
   }
   if constexpr (OP == kOpRealize) return;
   const int no = a.no;
-  // Outer (3-D, unrolled): rho_i at this lane's step-A positions, read once from
-  // Rsm into registers for all nine products (instead of two shared loads per
-  // element per output pair)
-// Outer op: 1 = compile-time products with rho in registers (rreg), 2 = the
-// same with rho read from shared memory, 0 = runtime output loop.  A/B (r02):
-// 2 with 6 CTAs/SM: outer z-lines 2.13 -> 1.90 ms, deformation GN HVP 9.52 ->
-// 9.31 ms (1 spills at 6 CTAs/SM and ties 0)
-#ifndef BLR_ZUNROLL_OUTER
-#define BLR_ZUNROLL_OUTER 2
-#endif
-  constexpr bool kUnrollOuter = BLR_ZUNROLL_OUTER != 0 && OP == kOpOuter;
-  // BLR_ZUNROLL_OUTER=2: compile-time products but rho read from Rsm (no rreg)
-  constexpr bool kOuterRreg = BLR_ZUNROLL_OUTER == 1;
-  T rreg[kUnrollOuter && kOuterRreg ? 3 : 1][kUnrollOuter && kOuterRreg ? S::R1 : 1];
-  const bool outer3 = kUnrollOuter && a.d == 3 && no == 9;
-  if constexpr (kUnrollOuter && kOuterRreg) {
-    if (outer3) {
-      __syncwarp();
-      const int la = lane / S::R2, n2a = lane - (lane / S::R2) * S::R2;
-      const bool oka = la < nl && la < S::LPW;
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int n1 = 0; n1 < S::R1; ++n1) rreg[i][n1] = oka ? Rsm[i * ldR + la * LR + S::R2 * n1 + n2a] : (T)0;
-    }
-  }
+  // Outer (3-D): the five output pairs unrolled, so each product's rho / V
+  // slots are compile-time constants (rho read from Rsm; holding it in
+  // registers spills at 6 CTAs/SM).  A/B (r02): outer z-lines 2.13 -> 1.90 ms,
+  // deformation GN HVP 9.52 -> 9.31 ms.
+  const bool outer3 = OP == kOpOuter && a.d == 3 && no == 9;
   // One output pair (o, o + 1).  OS >= 0: o is a compile-time constant.
   auto out_step = [&](int o, auto oc) {
     constexpr int OS = decltype(oc)::value;
@@ -1183,15 +943,10 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
 #pragma unroll
         for (int k2 = 0; k2 < S::R2; ++k2) {
           T v1 = 0, v2 = 0;
-          if constexpr (OS >= 100) {  // compile-time output pair (OS - 100, OS - 99)
-            v1 = acc[OS - 100][k2];
-            if constexpr (OS - 99 < NOM) v2 = acc[OS - 99][k2];
-          } else {
 #pragma unroll
-            for (int q = 0; q < NOM; ++q) {
-              if (q == o) v1 = acc[q][k2];
-              if (q == o + 1) v2 = acc[q][k2];
-            }
+          for (int q = 0; q < NOM; ++q) {
+            if (q == o) v1 = acc[q][k2];
+            if (q == o + 1) v2 = acc[q][k2];
           }
           BLR_CHECK(bl * LX + k1 + S::R1 * k2 < stage_n, "zlines xbuf acc");
           xbuf[bl * LX + k1 + S::R1 * k2] = cx<T>(v1, v2);
@@ -1207,15 +962,11 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
     auto load = [&](int line, int z, int n1) -> Cx<T> {
       if constexpr (Tr::acc) {
         return xbuf[line * LX + z];
-      } else if constexpr (OP == kOpOuter && OS >= 0 && OS < 100) {
+      } else if constexpr (OP == kOpOuter && OS >= 0) {
         constexpr int I1 = OS / 3, J1 = OS % 3, I2 = (OS + 1) / 3, J2 = (OS + 1) % 3;
-        if constexpr (kOuterRreg) {
-          return cx<T>(rreg[I1][n1] * vreg[J1][n1], OS + 1 < 9 ? rreg[I2 < 3 ? I2 : 0][n1] * vreg[J2][n1] : (T)0);
-        } else {
-          const int li = line * LR + z;
-          return cx<T>(Rsm[I1 * ldR + li] * vreg[J1][n1],
-                       OS + 1 < 9 ? Rsm[(I2 < 3 ? I2 : 0) * ldR + li] * vreg[J2][n1] : (T)0);
-        }
+        const int li = line * LR + z;
+        return cx<T>(Rsm[I1 * ldR + li] * vreg[J1][n1],
+                     OS + 1 < 9 ? Rsm[(I2 < 3 ? I2 : 0) * ldR + li] * vreg[J2][n1] : (T)0);
       } else if constexpr (OP == kOpOuter) {
         const int li = line * LR + z;
         const T v1 = oj1 == 0 ? vreg[0][n1] : (oj1 == 1 ? vreg[1][n1] : vreg[2][n1]);
@@ -1235,12 +986,9 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
     wfft<T, S, false>(tile, twp, nl, load, store);
     Cx<T>* O1 = a.sout[o] + sline;
     Cx<T>* O2 = two ? a.sout[o + 1] + sline : nullptr;
-// A/B (r02): the fixed-trip extraction is -1.4% on the deformation GN HVP
-// (9.64 -> 9.51 ms); compile-time ACC output slots (BLR_ZOUT_UNROLL) +1.4%
-#ifndef BLR_ZEXT_UNROLL
-#define BLR_ZEXT_UNROLL 1
-#endif
-    if constexpr (BLR_ZEXT_UNROLL && BLR_PF_OFFS) {
+    {
+      // A/B (r02): the fixed-trip extraction is -1.4% on the deformation GN HVP
+      // (9.64 -> 9.51 ms) against a strided idx loop
       // fixed-trip extraction over the prefetch slots (same (k, l) mapping and
       // global offsets): all shared loads of the warp's rows can be in flight
       Cx<T> Zs[kPfSlots], Zms[kPfSlots];
@@ -1255,42 +1003,23 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
 #pragma unroll
       for (int j = 0; j < kPfSlots; ++j) {
         if (pf_off[j] < 0) continue;
+        BLR_CHECK(sline + pf_off[j] < g.ns, "zlines out");
         const Cx<T> Z = Zs[j];
         Cx<T> Zm = Zms[j];
         Zm.y = -Zm.y;
         O1[pf_off[j]] = cx<T>((T)0.5 * (Z.x + Zm.x), (T)0.5 * (Z.y + Zm.y));
         if (two) O2[pf_off[j]] = cx<T>((T)0.5 * (Z.y - Zm.y), (T)-0.5 * (Z.x - Zm.x));
       }
-    } else {
-      for (int idx = lane; idx < S::LPW * Kz1; idx += 32) {
-        const int k = idx / S::LPW, l = idx - (idx / S::LPW) * S::LPW;  // compile-time divisor
-        if (l >= nl) continue;
-        BLR_CHECK(sline + k * kzs + l < g.ns && l * LX + k < stage_n, "zlines out");
-        const Cx<T> Z = xbuf[l * LX + k];
-        Cx<T> Zm = xbuf[l * LX + (k == 0 ? 0 : L - k)];
-        Zm.y = -Zm.y;
-        O1[k * kzs + l] = cx<T>((T)0.5 * (Z.x + Zm.x), (T)0.5 * (Z.y + Zm.y));
-        if (two) O2[k * kzs + l] = cx<T>((T)0.5 * (Z.y - Zm.y), (T)-0.5 * (Z.x - Zm.x));
-      }
     }
     __syncwarp();
   };
-#ifndef BLR_ZOUT_UNROLL
-#define BLR_ZOUT_UNROLL 0
-#endif
-  constexpr bool kUnrollAccOut = BLR_ZOUT_UNROLL && Tr::acc && OP != kOpContract && NOM == 3;
   if (outer3) {
-    if constexpr (kUnrollOuter) {
+    if constexpr (OP == kOpOuter) {
       out_step(0, std::integral_constant<int, 0>{});
       out_step(2, std::integral_constant<int, 2>{});
       out_step(4, std::integral_constant<int, 4>{});
       out_step(6, std::integral_constant<int, 6>{});
       out_step(8, std::integral_constant<int, 8>{});
-    }
-  } else if (kUnrollAccOut && no == 3) {
-    if constexpr (kUnrollAccOut) {  // compile-time output slots: no selects over the accumulators
-      out_step(0, std::integral_constant<int, 100>{});
-      out_step(2, std::integral_constant<int, 102>{});
     }
   } else {
     for (int o = 0; o < no; o += 2) out_step(o, std::integral_constant<int, -1>{});
@@ -1400,69 +1129,6 @@ __global__ void __launch_bounds__(kPWF * 32, BLR_YFWD_MINB) k_yfwd(YFwdArgs<T> a
   }
 }
 
-// Lean one-shot forward y pass (BLR_YFWD_LEAN=1), shaped like the inverse
-// passes: one CTA per (job, kz, chunk of kPW * LPW x rows), rows staged with
-// per-element cp.async, the FFT tile overlaying each warp's own rows, the
-// job's terms summed in registers and the in-band outputs stored straight from
-// the registers to the I layout -- no shared accumulator, no persistent loop.
-#ifndef BLR_YFWD_LEAN_MINB
-#define BLR_YFWD_LEAN_MINB 0
-#endif
-template <typename T, class S>
-__global__ void __launch_bounds__(kPW * 32, BLR_YFWD_LEAN_MINB) k_yfwd_lean(YFwdArgs<T> a, PadGeom g, const double* __restrict__ twg) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int LPC = kPW * S::LPW;
-  constexpr int LS = row_stride<T, S, true>();
-  const int P0 = g.P[0], K1 = g.K[1], B1 = g.B[1];
-  T* tw = (T*)smem_raw;
-  Cx<T>* slab = (Cx<T>*)(tw + 2 * S::L);  // [LPC][LS]
-  const int nxb = (P0 + LPC - 1) / LPC;
-  const int per = g.Kz1 * nxb;
-  const int jb = blockIdx.x / per;
-  const int r = blockIdx.x - jb * per;
-  const int kz = r / nxb;
-  const int cx0 = (r - kz * nxb) * LPC;
-  const int nlc = min(LPC, P0 - cx0);
-  const int nt = a.nterms[jb];
-  const int wl0 = (threadIdx.x >> 5) * S::LPW;
-  const int nl = min(S::LPW, nlc - wl0);
-  const T kzk = (T)(kTwoPi * (double)kz);
-  load_tw_async<T>(tw, twg, S::L);
-  pdl_wait();
-  Cx<T> yacc[S::R2];
-  Cx<T>* out = a.out + jb * g.n1 + (int64_t)kz * B1 * P0 + cx0 + wl0;  // + iy * P0 + line
-  for (int t = 0; t < nt; ++t) {
-    const Cx<T>* src = a.sin[jb][t] + ((int64_t)kz * P0 + cx0) * S::L;  // nlc contiguous rows
-    for (int i = threadIdx.x; i < nlc * S::L; i += blockDim.x) {
-      const int row = i / S::L, col = i - (i / S::L) * S::L;  // compile-time divisor
-      cp_async<T>(slab + row * LS + col, src + i);
-    }
-    __pipeline_commit();
-    __pipeline_wait_prior(0);
-    __syncthreads();
-    if (nl > 0) {
-      const int ax = a.axis[jb][t];
-      const Cx<T>* sl = slab + wl0 * LS;
-      auto load = [&](int line, int y, int) -> Cx<T> { return sl[line * LS + y]; };
-      auto store = [&](int line, int q, int k2, Cx<T> v) {
-        const int iy = bin_to_index(q, S::L, K1, B1);
-        if (iy >= 0) {
-          if (ax == 1) v = mul_ik<T>(v, (T)(kTwoPi * (double)freq_of(iy, K1, B1)));
-          else if (ax == 2) v = mul_ik<T>(v, kzk);
-        }
-        yacc[k2] = t == 0 ? v : cadd(yacc[k2], v);
-        if (t == nt - 1 && iy >= 0) {
-          BLR_CHECK(jb * g.n1 + (int64_t)kz * B1 * P0 + cx0 + wl0 + line + (int64_t)iy * P0 < a.nj * g.n1,
-                    "yfwd_lean out");
-          out[(int64_t)iy * P0 + line] = yacc[k2];
-        }
-      };
-      wfft<T, S, false, true>(slab + wl0 * LS, tw, nl, load, store);
-    }
-    if (t + 1 < nt) __syncthreads();  // the slab is refilled by the next term
-  }
-}
-
 // ---------------------------------------------------------------------------
 // forward x pass + epilogue: I [..][kz][ky][x] -> band, multipliers, 1/P^3,
 // -(v + .) / negation, fused RK4 stage update (kz = 0 symmetrized in-item)
@@ -1491,7 +1157,6 @@ struct FwdArgs {
   Cx<T>* cur;
   Cx<T>* acc;
   Cx<T>* stage;
-  Cx<T>* kres;      // deferred epilogue: x-pass results [no][nh] (k_xfwd_epi consumes them)
 };
 
 // Cooperative epilogue of one (output, kz, ky-chunk) block from the result
@@ -1561,11 +1226,10 @@ __device__ __forceinline__ void epilogue_block(const FwdArgs<T>& a, const FwdOut
 #ifndef BLR_XFWD_MINB
 #define BLR_XFWD_MINB 3
 #endif
-// DEFER: the x pass only writes its (scaled, kz = 0 symmetrized) results to
-// a.kres; the RK4 / -(v + .) epilogue runs in k_xfwd_epi, a streaming kernel at
-// full occupancy, so the transform kernel carries no epilogue registers.
-template <typename T, class S, bool DEFER = false>
-__global__ void __launch_bounds__(kPWF * 32, DEFER ? 6 : BLR_XFWD_MINB) k_xfwd(FwdArgs<T> a, PadGeom g, const double* __restrict__ twg) {
+// (deferring the epilogue to a streaming kernel: 156 instead of 226 registers
+// here, but A/B r02 x-forward 1.92 -> 2.04 ms per HVP)
+template <typename T, class S>
+__global__ void __launch_bounds__(kPWF * 32, BLR_XFWD_MINB) k_xfwd(FwdArgs<T> a, PadGeom g, const double* __restrict__ twg) {
   static_assert(kPWF == 2, "kz = 0 mirror items use one warp per half");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int LPW = S::LPW;
@@ -1670,7 +1334,7 @@ __global__ void __launch_bounds__(kPWF * 32, DEFER ? 6 : BLR_XFWD_MINB) k_xfwd(F
     if (ntt >= nt) { nit = it + gridDim.x; ntt = 0; }
     if (nit < nitems) issue(nit, ntt, b ^ 1);
     stg.commit();
-    if (!DEFER && t == 0) prefetch_epi(it);
+    if (t == 0) prefetch_epi(it);
     stg.wait(b);
     const Item m = decode(it - o * per);
     const int kz = m.kz;
@@ -1729,16 +1393,7 @@ __global__ void __launch_bounds__(kPWF * 32, DEFER ? 6 : BLR_XFWD_MINB) k_xfwd(F
         r = cscale(src[ix * LPCS + l], sc);
         return true;
       };
-      if constexpr (DEFER) {
-        for (int i = threadIdx.x; i < B0 * LPC; i += blockDim.x) {
-          const int ix = i / LPC, l = i - (i / LPC) * LPC;  // compile-time divisor
-          int64_t e;
-          Cx<T> r;
-          if (elem(ix, l, e, r)) a.kres[(int64_t)o * g.nh + e] = r;
-        }
-      } else {
-        epilogue_block<T, LPC>(a, O, o, g, elem);
-      }
+      epilogue_block<T, LPC>(a, O, o, g, elem);
     }
     __syncthreads();
     it = nit;
@@ -1854,10 +1509,6 @@ struct PadEngine {
   int line_smem_max = 0;
   void* buf[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t buf_bytes[4] = {0, 0, 0, 0};
-  // side stream for work that overlaps the latency-bound pass kernels
-  // (k_dudv, state_tangents_v2) and its double-buffer events
-  cudaStream_t aux = nullptr;
-  cudaEvent_t ev_start = nullptr, ev_q[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
 };
 
 
@@ -1923,7 +1574,7 @@ void launch_lines(blr_ctx* c, PadEngine* e, const LineArgs<T>& a) {
   const int ns_blk = OP == kOpContract ? a.d : a.ns;
   const int nreal = OP == kOpContract ? a.d : (ZOp<OP>::acc || OP == kOpRealize) ? 0 : ns_blk;
   const int nst = ZOp<OP>::acc ? a.nst : 0;
-  const size_t stage_n = std::max<size_t>(BLR_ZROW ? 4 * (size_t)(g.Kz1 + 1) * S::LPW : 4 * (size_t)g.Kz1 * S::LPW + S::LPW,
+  const size_t stage_n = std::max<size_t>(4 * (size_t)g.Kz1 * S::LPW + S::LPW,
                                           (size_t)S::LPW * ZLineG<T, S>::LX);
   const size_t warp_bytes = sizeof(Cx<T>) * ((size_t)TileG<T, S>::TILE + stage_n) +
                             sizeof(T) * (size_t)(nreal + nst) * S::LPW * ZLineG<T, S>::LR;
@@ -1943,23 +1594,11 @@ void launch_lines(blr_ctx* c, PadEngine* e, const LineArgs<T>& a) {
   launch_pdl(k_zlines<T, S, OP>, g.P[0] * nyc, kZWarps * 32, sm, c->stream, a, g, (const double*)e->tw[2]);
   BLR_LAUNCHED();
 }
-// A/B (r02): the lean one-shot y-forward ties the persistent one (1.77 vs 1.76
-// ms per HVP; 158 registers either way), so the persistent kernel stays
-#ifndef BLR_YFWD_LEAN
-#define BLR_YFWD_LEAN 0
-#endif
+// (a lean one-shot y-forward shaped like the inverse passes tied this
+// persistent kernel, A/B r02 1.77 vs 1.76 ms per HVP)
 template <typename T, class S>
 void launch_yfwd(blr_ctx* c, PadEngine* e, const YFwdArgs<T>& a) {
   const PadGeom& g = e->g;
-  if (BLR_YFWD_LEAN) {
-    constexpr int LPC = kPW * S::LPW;
-    const size_t sm = sizeof(T) * 2 * S::L + sizeof(Cx<T>) * (size_t)LPC * row_stride<T, S, true>();
-    ensure_smem(k_yfwd_lean<T, S>, sm);
-    const int nxb = (g.P[0] + LPC - 1) / LPC;
-    launch_pdl(k_yfwd_lean<T, S>, a.nj * g.Kz1 * nxb, kPW * 32, sm, c->stream, a, g, (const double*)e->tw[1]);
-    BLR_LAUNCHED();
-    return;
-  }
   constexpr int LPC = kPWF * S::LPW;
   const size_t sm = sizeof(Cx<T>) * (S::L + 2 * (size_t)LPC * fwd_row_stride<T, S>() +
                                      (size_t)g.B[1] * t_stride<LPC>());
@@ -1968,46 +1607,6 @@ void launch_yfwd(blr_ctx* c, PadEngine* e, const YFwdArgs<T>& a) {
   const int grid = persistent_grid(k_yfwd<T, S>, kPWF * 32, sm, a.nj * g.Kz1 * nxb, BLR_FWD_GRID_DIV);
   launch_pdl(k_yfwd<T, S>, grid, kPWF * 32, sm, c->stream, a, g, (const double*)e->tw[1]);
   BLR_LAUNCHED();
-}
-// the deferred x-pass epilogue: one thread per H-layout element of every output
-template <typename T>
-__global__ void __launch_bounds__(256) k_xfwd_epi(FwdArgs<T> a, PadGeom g) {
-  pdl_wait();
-  const int64_t n = (int64_t)a.no * g.nh;
-  const int s = a.rk_s;
-  for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < n; h += (int64_t)gridDim.x * blockDim.x) {
-    const int o = (int)(h / g.nh);
-    const int64_t e = h - (int64_t)o * g.nh;
-    const FwdOut<T>& O = a.o[o];
-    const Cx<T> r = a.kres[h];
-    Cx<T> k;
-    if (O.mode == kEpiNegAdd) {
-      const Cx<T> v = O.vt[e];
-      k = cx<T>(-(v.x + r.x), -(v.y + r.y));
-    } else if (O.mode == kEpiNeg) {
-      k = cx<T>(-r.x, -r.y);
-    } else {
-      k = r;
-    }
-    if (a.kout) a.kout[h] = k;
-    if (s) {
-      const Cx<T> cc = a.cur[h];
-      Cx<T> acv;
-      if (s == 1) {
-        acv = k;
-      } else {
-        const Cx<T> ac = a.acc[h];
-        const T m = s < 4 ? (T)2 : (T)1;
-        acv = cx<T>(ac.x + m * k.x, ac.y + m * k.y);
-      }
-      if (s < 4) {
-        a.acc[h] = acv;
-        a.stage[h] = cx<T>(cc.x + a.cs * k.x, cc.y + a.cs * k.y);
-      } else {
-        a.cur[h] = cx<T>(cc.x + a.h6 * acv.x, cc.y + a.h6 * acv.y);
-      }
-    }
-  }
 }
 
 template <typename T, class S>
@@ -2019,15 +1618,6 @@ void launch_xfwd(blr_ctx* c, PadEngine* e, const FwdArgs<T>& a) {
   const int nyb = (g.B[1] + LPC - 1) / LPC;
   const int n0 = (g.K[1] + 1 + S::LPW - 1) / S::LPW;
   const int items = a.no * (n0 + (g.Kz1 - 1) * nyb);
-  if (a.kres) {
-    ensure_smem(k_xfwd<T, S, true>, sm);
-    const int grid = persistent_grid(k_xfwd<T, S, true>, kPWF * 32, sm, items);
-    launch_pdl(k_xfwd<T, S, true>, grid, kPWF * 32, sm, c->stream, a, g, (const double*)e->tw[0]);
-    BLR_LAUNCHED();
-    launch_pdl(k_xfwd_epi<T>, grid_blocks((int64_t)a.no * g.nh, 256, 148 * 8), 256, 0, c->stream, a, g);
-    BLR_LAUNCHED();
-    return;
-  }
   ensure_smem(k_xfwd<T, S>, sm);
   const int grid = persistent_grid(k_xfwd<T, S>, kPWF * 32, sm, items, BLR_FWD_GRID_DIV);
   launch_pdl(k_xfwd<T, S>, grid, kPWF * 32, sm, c->stream, a, g, (const double*)e->tw[0]);
