@@ -473,6 +473,9 @@ template <int OP> struct ZOp {
 };
 
 constexpr int kZWarps = 2;
+#ifndef BLR_ZTW_ASYNC
+#define BLR_ZTW_ASYNC 1
+#endif
 // Occupancy targets (CTAs per SM) of the z-line kernel per op; 0 = registers
 // unconstrained.  The outer op is held at 6 CTAs per SM (its shared-memory
 // limit with the unrolled outer products).
@@ -614,9 +617,13 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
   // fp64: twiddles straight from the engine's global table (L1-resident), which
   // keeps the CTA's shared footprint at 6 CTAs per SM; fp32 converts into smem
   // register-bound ACC ops keep the twiddles in (otherwise unused) shared memory
+  // fp64 ACC ops: each warp copies the table into its own shared copy with
+  // cp.async before griddepcontrol.wait; the copies join the first prefetch
+  // group, so no CTA barrier and no register round trip at kernel start
   constexpr bool kTwG = sizeof(T) == 8 && !(Tr::acc && OP != kOpContract);
-  constexpr int kTwN = kTwG ? 0 : L;
-  T* tw = (T*)smem_raw;
+  constexpr bool kTwAsync = !kTwG && sizeof(T) == 8 && BLR_ZTW_ASYNC;
+  constexpr int kTwN = kTwG ? 0 : (kTwAsync ? kZWarps * L : L);
+  T* tw = (T*)smem_raw + (kTwAsync ? warp * 2 * L : 0);
   const T* twp = kTwG ? reinterpret_cast<const T*>(twz_g) : tw;
   unsigned char* wb = smem_raw + sizeof(Cx<T>) * kTwN + warp * warp_bytes;  // kTwN complex = 2 kTwN T
   Cx<T>* tile = (Cx<T>*)wb;
@@ -625,12 +632,15 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
   T* Vst = (T*)(stage + stage_n);
   T* Rsm = Vst + nst * S::LPW * LR;
   const int ldR = S::LPW * LR;
-  if constexpr (!kTwG) {
+  const int nl = min(S::LPW, P1 - y0);
+  if constexpr (kTwAsync) {
+    if (nl <= 0) return;
+    for (int i = lane; i < L; i += 32) __pipeline_memcpy_async(tw + 2 * i, twz_g + 2 * i, 16);
+  } else if constexpr (!kTwG) {
     load_tw<T>(tw, twz_g, L);
     __syncthreads();
   }
   pdl_wait();
-  const int nl = min(S::LPW, P1 - y0);
   if (nl <= 0) return;
   const int64_t sline = (int64_t)x * P1 + y0;
   const int64_t kzs = (int64_t)P0 * P1;
@@ -706,7 +716,7 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
     pf_off[j] = (i < Kz1 * S::LPW && l < nl) ? k * (int)kzs + l : -1;
   }
   auto prefetch = [&](int q) {
-    const int node = q / npair, p = q - node * npair;
+    const int node = OP == kOpContract ? q / npair : 0, p = q - node * npair;  // one node unless contracting
     const int64_t noff = OP == kOpContract ? node * a.sin_node_stride : 0;
     Cx<T>* st = stage + (q & 1) * 2 * fstride;
     for (int ff = 0; ff < 2; ++ff) {
@@ -806,7 +816,7 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
       __pipeline_wait_prior(0);
     }
     __syncwarp();
-    const int node = q / npair, p = q - node * npair;
+    const int node = OP == kOpContract ? q / npair : 0, p = q - node * npair;  // one node unless contracting
     const int f = 2 * p;
     const bool two = f + 1 < ns_blk;
     const int st1o = (q & 1) * 2 * fstride, st2o = st1o + fstride;
@@ -1579,7 +1589,8 @@ void launch_lines(blr_ctx* c, PadEngine* e, const LineArgs<T>& a) {
   const size_t warp_bytes = sizeof(Cx<T>) * ((size_t)TileG<T, S>::TILE + stage_n) +
                             sizeof(T) * (size_t)(nreal + nst) * S::LPW * ZLineG<T, S>::LR;
   const bool twg = sizeof(T) == 8 && !(ZOp<OP>::acc && OP != kOpContract);  // as kTwG in the kernel
-  const size_t sm = (twg ? 0 : S::L * sizeof(Cx<T>)) + kZWarps * warp_bytes;
+  const bool twa = !twg && sizeof(T) == 8 && BLR_ZTW_ASYNC;  // as kTwAsync: a table per warp
+  const size_t sm = (twg ? 0 : (twa ? kZWarps : 1) * S::L * sizeof(Cx<T>)) + kZWarps * warp_bytes;
   if (sm > (size_t)e->line_smem_max) throw Error(1, "z-line kernel shared memory exceeds the device limit");
   static bool attr_done[2] = {false, false};
   if (!attr_done[sizeof(T) == 8 ? 0 : 1]) {
