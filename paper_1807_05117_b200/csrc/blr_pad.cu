@@ -106,8 +106,14 @@ static PadEngine* engine(blr_ctx* c) {
         tw[k1 * R2 + n2] = co;
         tw[L + k1 * R2 + n2] = s;
       }
-    BLR_CUDA(cudaMalloc(&e.tw[a], 2 * (size_t)L * sizeof(double)));
-    BLR_CUDA(cudaMemcpy(e.tw[a], tw.data(), 2 * (size_t)L * sizeof(double), cudaMemcpyHostToDevice));
+    // followed by the same table rounded to fp32 (2 L floats), so fp32 kernels
+    // can stage it with cp.async instead of converting element by element
+    std::vector<float> twf(2 * (size_t)L);
+    for (size_t i = 0; i < twf.size(); ++i) twf[i] = (float)tw[i];
+    const size_t nb = 2 * (size_t)L * sizeof(double);
+    BLR_CUDA(cudaMalloc(&e.tw[a], nb + 2 * (size_t)L * sizeof(float)));
+    BLR_CUDA(cudaMemcpy(e.tw[a], tw.data(), nb, cudaMemcpyHostToDevice));
+    BLR_CUDA(cudaMemcpy((char*)e.tw[a] + nb, twf.data(), twf.size() * sizeof(float), cudaMemcpyHostToDevice));
   }
   e.ok = true;
   return &e;

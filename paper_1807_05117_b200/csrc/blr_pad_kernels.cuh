@@ -57,18 +57,27 @@ template <typename T>
 __device__ __forceinline__ void load_tw(T* dst, const double* src, int L) {
   for (int i = threadIdx.x; i < 2 * L; i += blockDim.x) dst[i] = (T)src[i];
 }
-// fp64: the same as cp.async 16-byte copies in the caller's open cp.async
-// group (no register round trip; the caller commits and waits); fp32 converts
-// synchronously.  Returns true when copies were issued.  Used by the inverse
-// passes, issued before griddepcontrol.wait (A/B r02: y-inverse 1.49 -> 1.45 ms
-// per HVP).
+// The same as cp.async copies in the caller's open cp.async group (no register
+// round trip; the caller commits and waits): fp64 16-byte copies of the table,
+// fp32 8-byte copies of the fp32 table stored after it (blr_pad.cu engine
+// set-up).  Threads `first`, `first + stride`, ... issue.  Used before
+// griddepcontrol.wait (A/B r02: y-inverse 1.49 -> 1.45 ms per HVP).
 #ifndef BLR_TW_ASYNC
 #define BLR_TW_ASYNC 1
 #endif
 template <typename T>
+__device__ __forceinline__ void copy_tw_async(T* dst, const double* src, int L, int first, int stride) {
+  if constexpr (sizeof(T) == 8) {
+    for (int i = first; i < L; i += stride) __pipeline_memcpy_async(dst + 2 * i, src + 2 * i, 16);
+  } else {
+    const float* f = reinterpret_cast<const float*>(src + 2 * L);
+    for (int i = first; i < L; i += stride) __pipeline_memcpy_async(dst + 2 * i, f + 2 * i, 8);
+  }
+}
+template <typename T>
 __device__ __forceinline__ bool load_tw_async(T* dst, const double* src, int L) {
-  if constexpr (sizeof(T) == 8 && BLR_TW_ASYNC) {
-    for (int i = threadIdx.x; i < L; i += blockDim.x) __pipeline_memcpy_async(dst + 2 * i, src + 2 * i, 16);
+  if constexpr (BLR_TW_ASYNC) {
+    copy_tw_async<T>(dst, src, L, threadIdx.x, blockDim.x);
     return true;
   } else {
     load_tw<T>(dst, src, L);
@@ -617,11 +626,11 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
   // fp64: twiddles straight from the engine's global table (L1-resident), which
   // keeps the CTA's shared footprint at 6 CTAs per SM; fp32 converts into smem
   // register-bound ACC ops keep the twiddles in (otherwise unused) shared memory
-  // fp64 ACC ops: each warp copies the table into its own shared copy with
+  // shared twiddles: each warp copies the table into its own shared copy with
   // cp.async before griddepcontrol.wait; the copies join the first prefetch
   // group, so no CTA barrier and no register round trip at kernel start
   constexpr bool kTwG = sizeof(T) == 8 && !(Tr::acc && OP != kOpContract);
-  constexpr bool kTwAsync = !kTwG && sizeof(T) == 8 && BLR_ZTW_ASYNC;
+  constexpr bool kTwAsync = !kTwG && BLR_ZTW_ASYNC;
   constexpr int kTwN = kTwG ? 0 : (kTwAsync ? kZWarps * L : L);
   T* tw = (T*)smem_raw + (kTwAsync ? warp * 2 * L : 0);
   const T* twp = kTwG ? reinterpret_cast<const T*>(twz_g) : tw;
@@ -635,7 +644,7 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
   const int nl = min(S::LPW, P1 - y0);
   if constexpr (kTwAsync) {
     if (nl <= 0) return;
-    for (int i = lane; i < L; i += 32) __pipeline_memcpy_async(tw + 2 * i, twz_g + 2 * i, 16);
+    copy_tw_async<T>(tw, twz_g, L, lane, 32);
   } else if constexpr (!kTwG) {
     load_tw<T>(tw, twz_g, L);
     __syncthreads();
@@ -1589,7 +1598,7 @@ void launch_lines(blr_ctx* c, PadEngine* e, const LineArgs<T>& a) {
   const size_t warp_bytes = sizeof(Cx<T>) * ((size_t)TileG<T, S>::TILE + stage_n) +
                             sizeof(T) * (size_t)(nreal + nst) * S::LPW * ZLineG<T, S>::LR;
   const bool twg = sizeof(T) == 8 && !(ZOp<OP>::acc && OP != kOpContract);  // as kTwG in the kernel
-  const bool twa = !twg && sizeof(T) == 8 && BLR_ZTW_ASYNC;  // as kTwAsync: a table per warp
+  const bool twa = !twg && BLR_ZTW_ASYNC;  // as kTwAsync: a table per warp
   const size_t sm = (twg ? 0 : (twa ? kZWarps : 1) * S::L * sizeof(Cx<T>)) + kZWarps * warp_bytes;
   if (sm > (size_t)e->line_smem_max) throw Error(1, "z-line kernel shared memory exceeds the device limit");
   static bool attr_done[2] = {false, false};
