@@ -3,6 +3,8 @@
 // (kernels: blr_pad_kernels.cuh, instantiated per length in blr_pad_L*.cu).
 #include "blr_pad_kernels.cuh"
 
+#include <atomic>
+
 #include <array>
 #include <cmath>
 #include <cstring>
@@ -179,16 +181,19 @@ static void dispatch_xfwd(blr_ctx* c, PadEngine* e, const FwdArgs<T>& a) {
 // one-job outputs (state GN HVP 5.59 vs 5.43 ms) and loses for the flux
 // divergence (2 jobs, 93 KB smem -> 2 CTAs/SM: deformation 11.4 vs 9.76 ms);
 // ncu: exposed bulk-load and cluster-barrier waits (no double buffering).
-static int g_fwd2_disabled = -1;
-void set_fused_forward(int on) { g_fwd2_disabled = on ? 0 : 1; }
+static std::atomic<int> g_fwd2_disabled{-1};  // -1: not yet read from BLR_FWD2
+void set_fused_forward(int on) { g_fwd2_disabled.store(on ? 0 : 1); }
 template <typename T>
 static bool dispatch_fwd2(blr_ctx* c, PadEngine* e, const Fwd2Args<T>& a, int no, int njmax, bool run) {
-  if (g_fwd2_disabled < 0) {
+  int dis = g_fwd2_disabled.load();
+  if (dis < 0) {
     const char* env = getenv("BLR_FWD2");
-    g_fwd2_disabled = (env && env[0] == '1') ? 0 : 1;
+    int expect = -1;
+    g_fwd2_disabled.compare_exchange_strong(expect, (env && env[0] == '1') ? 0 : 1);
+    dis = g_fwd2_disabled.load();
   }
   const PadGeom& g = e->g;
-  if (g_fwd2_disabled || g.P[0] != g.P[1] || g.P[0] < 2) return false;
+  if (dis || g.P[0] != g.P[1] || g.P[0] < 2) return false;
   switch (g.P[0]) {
 #define X(LL, A, B)                                                  \
   case LL:                                                           \

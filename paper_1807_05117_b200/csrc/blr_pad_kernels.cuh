@@ -25,6 +25,8 @@
 
 #include <cmath>
 #include <array>
+#include <map>
+#include <mutex>
 #include <cstring>
 #include <utility>
 #include <type_traits>
@@ -1531,38 +1533,60 @@ struct PadEngine {
 };
 
 
-// raise the kernel's dynamic shared-memory limit once (not per launch)
+// Per-kernel launch facts, computed once per (kernel, shared bytes): kernels
+// of one signature share a function-pointer type, so these are keyed by the
+// kernel's address, not by template statics; the mutex makes the first use
+// safe when several host threads launch concurrently.
+struct KernelFacts {
+  std::mutex mu;
+  std::map<std::pair<const void*, size_t>, int> occupancy;  // CTAs per SM
+  std::map<const void*, bool> smem_raised;
+  int nsm = 0;
+};
+inline KernelFacts& kernel_facts() {
+  static KernelFacts f;
+  return f;
+}
+
 // forward-pass persistent grids: at most per_sm * nsm / BLR_FWD_GRID_DIV CTAs
 #ifndef BLR_FWD_GRID_DIV
 #define BLR_FWD_GRID_DIV 1
 #endif
 template <class K>
 static int persistent_grid(K kernel, int threads, size_t smem, int nitems, int div = 1) {
-  static int per_sm = 0;  // one static per kernel instantiation (smem is fixed per instantiation)
-  static int nsm = 0;
-  if (!per_sm) {
+  KernelFacts& f = kernel_facts();
+  std::lock_guard<std::mutex> lk(f.mu);
+  if (!f.nsm) {
     int dev;
     BLR_CUDA(cudaGetDevice(&dev));
-    BLR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    BLR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
-    if (per_sm < 1) per_sm = 1;
+    BLR_CUDA(cudaDeviceGetAttribute(&f.nsm, cudaDevAttrMultiProcessorCount, dev));
   }
-  return std::max(1, std::min(nitems, per_sm * nsm / div));
+  const auto key = std::make_pair((const void*)kernel, smem);
+  auto it = f.occupancy.find(key);
+  if (it == f.occupancy.end()) {
+    int per_sm = 0;
+    BLR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+    it = f.occupancy.emplace(key, std::max(per_sm, 1)).first;
+  }
+  return std::max(1, std::min(nitems, it->second * f.nsm / div));
 }
 
+// raise the kernel's dynamic shared-memory limit to the device maximum once
+// (not per launch) when it needs more than the default 48 KB
 template <typename K>
 static void ensure_smem(K kernel, size_t bytes) {
-  static size_t set = 48 * 1024;  // one static per kernel instantiation
-  if (bytes > set) {
-    int dev, maxsm;
-    BLR_CUDA(cudaGetDevice(&dev));
-    BLR_CUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    cudaFuncAttributes fa;
-    BLR_CUDA(cudaFuncGetAttributes(&fa, kernel));
-    maxsm -= (int)fa.sharedSizeBytes;  // static shared memory (mbarriers) counts against the opt-in limit
-    BLR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
-    set = (size_t)maxsm;
-  }
+  if (bytes <= 48 * 1024) return;
+  KernelFacts& f = kernel_facts();
+  std::lock_guard<std::mutex> lk(f.mu);
+  if (f.smem_raised[(const void*)kernel]) return;
+  int dev, maxsm;
+  BLR_CUDA(cudaGetDevice(&dev));
+  BLR_CUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  cudaFuncAttributes fa;
+  BLR_CUDA(cudaFuncGetAttributes(&fa, kernel));
+  maxsm -= (int)fa.sharedSizeBytes;  // static shared memory (mbarriers) counts against the opt-in limit
+  BLR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+  f.smem_raised[(const void*)kernel] = true;
 }
 
 template <typename T, class S>
@@ -1601,14 +1625,7 @@ void launch_lines(blr_ctx* c, PadEngine* e, const LineArgs<T>& a) {
   const bool twa = !twg && BLR_ZTW_ASYNC;  // as kTwAsync: a table per warp
   const size_t sm = (twg ? 0 : (twa ? kZWarps : 1) * S::L * sizeof(Cx<T>)) + kZWarps * warp_bytes;
   if (sm > (size_t)e->line_smem_max) throw Error(1, "z-line kernel shared memory exceeds the device limit");
-  static bool attr_done[2] = {false, false};
-  if (!attr_done[sizeof(T) == 8 ? 0 : 1]) {
-    cudaFuncAttributes fa;
-    BLR_CUDA(cudaFuncGetAttributes(&fa, k_zlines<T, S, OP>));  // static shared memory counts too
-    BLR_CUDA(cudaFuncSetAttribute(k_zlines<T, S, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  e->line_smem_max - (int)fa.sharedSizeBytes));
-    attr_done[sizeof(T) == 8 ? 0 : 1] = true;
-  }
+  ensure_smem(k_zlines<T, S, OP>, sm);
   constexpr int LPC = kZWarps * S::LPW;
   const int nyc = (g.P[1] + LPC - 1) / LPC;
   launch_pdl(k_zlines<T, S, OP>, g.P[0] * nyc, kZWarps * 32, sm, c->stream, a, g, (const double*)e->tw[2]);

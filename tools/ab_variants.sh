@@ -10,7 +10,7 @@ for rep in 1 2; do
   for lib in $libs; do
     for o in deformation state; do
       BLR_LIB_PATH=$lib python bench.py --steps 40 --warmup 5 --cpu-baseline 0 --registration 0 --objective $o 2>/dev/null | tail -1 | \
-        python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$rep', '$lib'.split('/')[-2], '$o', round(d['ms_per_step'],3), 'ms', 'e2e', round(d['e2e']['value'],2), 'value', round(d['value'],2), d['clocks']['sm_mhz'])"
+        python -c "import json,sys; d=json.loads(sys.stdin.read()); kb=d.get('kernel_breakdown',{}); print('$rep', '$lib'.split('/')[-2], '$o', round(d['ms_per_step'],3), 'ms', 'e2e', round(d['e2e']['value'],2), 'value', round(d['value'],2), d['clocks']['sm_mhz'], ' '.join(k.replace('pad_','')+'='+str(round(v['ms'],3)) for k,v in kb.items() if v['ms']>0.5))"
     done
   done
 done
