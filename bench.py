@@ -435,13 +435,19 @@ def run_b200(args, rank, world, local):
     # record_stream (product buffers held by the copy stream) is first-use set-up
     hv = pipelined(max(args.warmup, 2))
     torch.cuda.synchronize()
-    barrier(world)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    hv = pipelined(args.steps)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    local_e2e_ms = e0.elapsed_time(e1)
+    # three repetitions of the K-step loop, the median reported (all three are
+    # in the line): one host hiccup of ~0.1 s inside a 0.2 s region was seen
+    # on a fresh box (tools/e2e_probe.py), and it is not the path's cost
+    e2e_reps = []
+    for _ in range(3):
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        hv = pipelined(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_reps.append(e0.elapsed_time(e1))
+    local_e2e_ms = float(np.median(e2e_reps))
     e2e_ms = max_over_ranks(local_e2e_ms, world)
     e2e_value = world * args.steps / (e2e_ms / 1e3)
     assert torch.equal(host_out, out.values.cpu()), "e2e result differs from the device-resident run"
@@ -517,7 +523,8 @@ def run_b200(args, rank, world, local):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64" if args.dtype == "float64" else "f32",
         "data": "synthetic (band_image pair + smooth v, w; SURVEY §8(d) recipe, seed 0)",
         "config": {**workload(args), "pad": list(dom.pad), "parallelism": f"replicas x{world}"},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": host_w.numel() * host_w.element_size(),
+        "e2e": {"value": e2e_value, "unit": UNIT, "reps_ms": [round(x, 3) for x in e2e_reps],
+                "h2d_bytes_per_step": host_w.numel() * host_w.element_size(),
                 "d2h_bytes_per_step": host_out.numel() * host_out.element_size()},
         "gpu_launches": launches,
         "roofline": roofline,
