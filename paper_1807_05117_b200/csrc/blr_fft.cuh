@@ -472,6 +472,9 @@ struct TileG {
 // twr[k1 * R2 + n2], imaginary parts at twr[L + k1 * R2 + n2].  Lanes of a
 // request differ in n2 only, so the two 8-byte (fp64) loads are conflict-free
 // (the packed table tw[k1 * n2] cost 2.4x the ideal wavefronts).
+#ifndef BLR_TW_SYM
+#define BLR_TW_SYM 2
+#endif
 template <typename T, class S>
 __device__ __forceinline__ Cx<T> twiddle(const T* twr, int k1, int n2) {
   return cx<T>(twr[k1 * S::R2 + n2], twr[S::L + k1 * S::R2 + n2]);
@@ -497,15 +500,48 @@ __device__ __forceinline__ void wfft_a(Cx<T>* tile, const T* twr, int nl, Load& 
     dft<T, S::R1, INV>(v);
     Cx<T>* t = tile + line * G::TS + n2;
     BLR_CHECK(line * G::TS + (S::R1 - 1) * G::KS + n2 < G::TILE, "wfft_a tile");
+    if constexpr (BLR_TW_SYM && S::R1 >= 4) {
+      // half the table loads: W^(k1 n2) for k1 <= M from the table, W^(R1 n2)
+      // from their products, and W^(k1 n2) = W^(R1 n2) conj(W^((R1 - k1) n2))
+      // for k1 > M (shared-memory / L1 loads traded for fp64 multiplies)
+      constexpr int M = (S::R1 + 1) / 2;
+      // BLR_TW_SYM >= 2: only k1 <= 5 - BLR_TW_SYM from the table, the rest of
+      // k1 <= M as products of two lower powers
+      constexpr int NLmax = BLR_TW_SYM >= 2 ? 5 - BLR_TW_SYM : M;
+      constexpr int NL = M > NLmax ? NLmax : M;
+      Cx<T> w[S::R1];
 #pragma unroll
-    for (int k1 = 0; k1 < S::R1; ++k1) {
-      Cx<T> z = v[k1];
-      if (k1 * n2 != 0) {
-        Cx<T> w = twiddle<T, S>(twr, k1, n2);
-        if (INV) w.y = -w.y;
-        z = cmul(z, w);
+      for (int k1 = 1; k1 <= NL; ++k1) w[k1] = twiddle<T, S>(twr, k1, n2);
+#pragma unroll
+      for (int k1 = NL + 1; k1 <= M; ++k1) w[k1] = cmul(w[k1 / 2], w[k1 - k1 / 2]);
+      const Cx<T> wr = S::R1 % 2 == 0 ? cmul(w[S::R1 / 2], w[S::R1 / 2]) : cmul(w[M - 1], w[M]);
+#pragma unroll
+      for (int k1 = M + 1; k1 < S::R1; ++k1) {
+        Cx<T> c = w[S::R1 - k1];
+        c.y = -c.y;
+        w[k1] = cmul(wr, c);
       }
-      t[k1 * G::KS] = z;
+#pragma unroll
+      for (int k1 = 0; k1 < S::R1; ++k1) {
+        Cx<T> z = v[k1];
+        if (k1 * n2 != 0) {
+          Cx<T> ww = w[k1 > 0 ? k1 : 1];
+          if (INV) ww.y = -ww.y;
+          z = cmul(z, ww);
+        }
+        t[k1 * G::KS] = z;
+      }
+    } else {
+#pragma unroll
+      for (int k1 = 0; k1 < S::R1; ++k1) {
+        Cx<T> z = v[k1];
+        if (k1 * n2 != 0) {
+          Cx<T> w = twiddle<T, S>(twr, k1, n2);
+          if (INV) w.y = -w.y;
+          z = cmul(z, w);
+        }
+        t[k1 * G::KS] = z;
+      }
     }
   }
   __syncwarp();

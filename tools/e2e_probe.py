@@ -66,6 +66,21 @@ def pipelined(n, marks=None):
     return hv
 
 
+import gc  # noqa: E402
+
+gc_log = []
+_gc_t = {}
+
+
+def _gc_cb(phase, info):
+    if phase == "start":
+        _gc_t["t"] = time.perf_counter()
+    else:
+        gc_log.append((info["generation"], (time.perf_counter() - _gc_t.get("t", time.perf_counter())) * 1e3,
+                       info.get("collected", 0)))
+
+
+gc.callbacks.append(_gc_cb)
 pipelined(3)
 torch.cuda.synchronize()
 for rep in range(a.reps):
@@ -84,6 +99,10 @@ for rep in range(a.reps):
     print(f"rep {rep}: {a.steps / tot * 1e3:.2f} HVP/s total {tot:.1f} ms | HVP ms min {min(hvp):.2f} med "
           f"{np.median(hvp):.2f} max {max(hvp):.2f} | gap ms max {max(gaps):.2f} sum {sum(gaps):.2f} | host ms "
           f"med {np.median(host):.2f} max {max(host):.2f} (step {int(np.argmax(host))}) | clocks {clk.summary()}")
+    slow = [(g, round(ms, 1)) for g, ms, _ in gc_log if ms > 2.0]
+    print("   gc: %d collections (gen2: %d), slow (gen, ms): %s" % (
+        len(gc_log), sum(1 for g, _, _ in gc_log if g == 2), slow))
+    gc_log.clear()
     st1 = torch.cuda.memory_stats()
     print("   allocator: segments +%d, cudaMalloc retries +%d, reserved %.2f GB" % (
         st1["segment.all.allocated"] - st0["segment.all.allocated"],
