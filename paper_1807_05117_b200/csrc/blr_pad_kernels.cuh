@@ -1054,6 +1054,14 @@ __global__ void __launch_bounds__(kZWarps * 32, zline_min_blocks(OP)) k_zlines(L
 // (after the transform) or i k_z.  Flux divergence folds its y and z terms
 // into one job; the x term needs i k_x after the x pass and stays separate.
 constexpr int kMaxYF = 24;
+// forward passes: twiddles by cp.async in flight with the first slab -- fp32
+// only; A/B r02: fp32 x / y forward 1.68 / 1.47 -> 1.61 / 1.43 ms, but fp64
+// 1.83 / 1.69 -> 1.89 / 1.85 ms (the synchronous fp64 load stays)
+#ifndef BLR_FWD_TW_ASYNC
+#define BLR_FWD_TW_ASYNC 1
+#endif
+template <typename T>
+constexpr bool fwd_tw_async() { return BLR_FWD_TW_ASYNC != 0 && sizeof(T) == 4; }
 template <typename T>
 struct YFwdArgs {
   const Cx<T>* sin[kMaxYF][3];
@@ -1097,13 +1105,20 @@ __global__ void __launch_bounds__(kPWF * 32, BLR_YFWD_MINB) k_yfwd(YFwdArgs<T> a
     stg.begin(b, (uint32_t)(nlc * S::L * sizeof(Cx<T>)));
     stg.rows(slab + b * SLAB, LS, src, S::L, nlc, S::L, b);
   };
-  load_tw<T>(tw, twg, S::L);  // (cp.async here: A/B r02 +1% on the forward passes)
+  // twiddles by cp.async in their own group, in flight with the first slab
+  if constexpr (fwd_tw_async<T>()) {
+    copy_tw_async<T>(tw, twg, S::L, threadIdx.x, blockDim.x);
+    __pipeline_commit();
+  } else {
+    load_tw<T>(tw, twg, S::L);
+  }
   int it = blockIdx.x, t = 0, b = 0;
   pdl_trigger();  // persistent grid: every CTA is already resident
   pdl_wait();
   if (it < nitems) issue(it, 0, 0);
   stg.commit();
   const int wl0 = (threadIdx.x >> 5) * S::LPW;
+  if constexpr (fwd_tw_async<T>()) __pipeline_wait_prior(decltype(stg)::kBulk ? 0 : 1);
   __syncthreads();  // twiddles
   while (it < nitems) {
     const int jb = it / per;
@@ -1338,7 +1353,12 @@ __global__ void __launch_bounds__(kPWF * 32, BLR_XFWD_MINB) k_xfwd(FwdArgs<T> a,
       }
     }
   };
-  load_tw<T>(tw, twg, S::L);  // (cp.async here: A/B r02 +1% on the forward passes)
+  if constexpr (fwd_tw_async<T>()) {  // as k_yfwd
+    copy_tw_async<T>(tw, twg, S::L, threadIdx.x, blockDim.x);
+    __pipeline_commit();
+  } else {
+    load_tw<T>(tw, twg, S::L);
+  }
   int it = blockIdx.x, t = 0, b = 0;
   pdl_trigger();  // persistent grid: every CTA is already resident
   pdl_wait();
@@ -1346,6 +1366,7 @@ __global__ void __launch_bounds__(kPWF * 32, BLR_XFWD_MINB) k_xfwd(FwdArgs<T> a,
   stg.commit();
   const int warp = threadIdx.x >> 5;
   const int wl0 = warp * LPW;
+  if constexpr (fwd_tw_async<T>()) __pipeline_wait_prior(decltype(stg)::kBulk ? 0 : 1);
   __syncthreads();  // twiddles
   while (it < nitems) {
     const int o = it / per;
