@@ -380,18 +380,28 @@ def run_b200(args, rank, world, local):
     torch.cuda.synchronize()
     barrier(world)
     stream = torch.cuda.current_stream()
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    l0 = _lib.launch_count()
+    # three timed windows of exactly K steps, each bracketed by a barrier and a
+    # synchronize; the median window is reported and all three are in the line
+    # (`windows_ms`): a host stall longer than the ~2 HVPs of queued launches
+    # idles the GPU, and such stalls (~0.1-0.3 s, rare, not the path's cost)
+    # were seen on fresh boxes
+    windows = []
+    launches = 0
     with Clocks(local) as clocks:
-        torch.cuda.synchronize()
-        start.record(stream)
-        for _ in range(args.steps):
-            out = ev.hessian_vector(w, gauss_newton=True)
-        end.record(stream)
-        torch.cuda.synchronize()
-    launches = (_lib.launch_count() - l0)
+        for _win in range(3):
+            barrier(world)
+            start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            l0 = _lib.launch_count()
+            torch.cuda.synchronize()
+            start.record(stream)
+            for _ in range(args.steps):
+                out = ev.hessian_vector(w, gauss_newton=True)
+            end.record(stream)
+            torch.cuda.synchronize()
+            launches = _lib.launch_count() - l0
+            windows.append(start.elapsed_time(end))
     barrier(world)
-    local_ms = start.elapsed_time(end)
+    local_ms = float(np.median(windows))
     t_ms = max_over_ranks(local_ms, world)
     per_step_ms = t_ms / args.steps
     value = world * args.steps / (t_ms / 1e3)
@@ -523,6 +533,7 @@ def run_b200(args, rank, world, local):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64" if args.dtype == "float64" else "f32",
         "data": "synthetic (band_image pair + smooth v, w; SURVEY §8(d) recipe, seed 0)",
         "config": {**workload(args), "pad": list(dom.pad), "parallelism": f"replicas x{world}"},
+        "windows_ms": [round(x, 3) for x in windows],
         "e2e": {"value": e2e_value, "unit": UNIT, "reps_ms": [round(x, 3) for x in e2e_reps],
                 "h2d_bytes_per_step": host_w.numel() * host_w.element_size(),
                 "d2h_bytes_per_step": host_out.numel() * host_out.element_size()},

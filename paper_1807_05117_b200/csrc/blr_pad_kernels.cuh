@@ -166,6 +166,39 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t bytes) {  // no arrive
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Inverse passes: the twiddle table lands by one cp.async.bulk on an mbarrier,
+// requested before griddepcontrol.wait (expect_tx without arrive); after the
+// slab's per-element cp.async copies are issued, thread 0 arrives and every
+// thread waits on the barrier (table) and its cp.async group (slab).  A/B r02:
+// deformation / state / fp32 GN HVP 8.64 / 4.90 / 6.07 -> 8.61 / 4.88 / 6.02
+// ms.  (Bulk copies for the slab rows too -- 12 lines x 16 B per row -- made
+// the fp64 y-inverse 1.38 -> 1.64 ms.)
+#ifndef BLR_INV_BULK
+#define BLR_INV_BULK 1
+#endif
+template <typename T, int L>
+constexpr bool inv_bulk_tw() { return BLR_INV_BULK && (2 * L * (int)sizeof(T)) % 16 == 0; }
+template <typename T, int L>
+__device__ __forceinline__ void inv_bulk_start(uint64_t* bar, T* tw, const double* twg) {
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t nb = 2 * L * sizeof(T);
+    mbar_expect_tx_only(bar, nb);
+    bulk_g2s(tw, sizeof(T) == 8 ? (const void*)twg : (const void*)(twg + 2 * L), nb, bar);
+  }
+}
+
 // Double-buffered slab staging for the persistent pass kernels.  fp64 rows are
 // whole 16-byte multiples: warp 0 arms the buffer's mbarrier with the byte
 // count and issues one cp.async.bulk per row (the copy engine writes the
@@ -304,16 +337,25 @@ __global__ void __launch_bounds__(kPW * 32) k_xinv(XPassArgs<T> a, PadGeom g, co
   const int cky0 = (r - kz * nyb) * LPC;
   const int nlc = min(LPC, B1 - cky0);
   const Cx<T>* src = a.src[xf] + ((int64_t)kz * B0) * B1 + cky0;
-  load_tw_async<T>(tw, twg, S::L);  // constant table: overlaps the predecessor's tail
+  constexpr bool kBulkTw = inv_bulk_tw<T, S::L>();
+  __shared__ uint64_t bar;
+  if constexpr (kBulkTw) inv_bulk_start<T, S::L>(&bar, tw, twg);
+  else load_tw_async<T>(tw, twg, S::L);  // constant table: overlaps the predecessor's tail
   pdl_wait();
-  for (int i = threadIdx.x; i < B0 * LPC; i += blockDim.x) {
-    const int ix = i / LPC, l = i - ix * LPC;
-    if (l < nlc) cp_async<T>(slab + ix * LPCS + l, src + ix * B1 + l);
-    BLR_CHECK(l >= nlc || (int64_t)kz * B0 * B1 + cky0 + ix * B1 + l < g.nh, "xinv src");
+  {
+    for (int i = threadIdx.x; i < B0 * LPC; i += blockDim.x) {
+      const int ix = i / LPC, l = i - ix * LPC;
+      if (l < nlc) cp_async<T>(slab + ix * LPCS + l, src + ix * B1 + l);
+      BLR_CHECK(l >= nlc || (int64_t)kz * B0 * B1 + cky0 + ix * B1 + l < g.nh, "xinv src");
+    }
+    __pipeline_commit();
+    if constexpr (kBulkTw) {
+      if (threadIdx.x == 0) mbar_arrive(&bar);  // the table's bytes complete the phase
+      mbar_wait(&bar, 0);
+    }
+    __pipeline_wait_prior(0);
+    __syncthreads();
   }
-  __pipeline_commit();
-  __pipeline_wait_prior(0);
-  __syncthreads();
   const int wl0 = (threadIdx.x >> 5) * S::LPW;
   const int nl = min(S::LPW, nlc - wl0);
   if (nl <= 0) return;
@@ -374,20 +416,29 @@ __global__ void __launch_bounds__(kPW * 32) k_yinv(YPassArgs<T> a, PadGeom g, co
   const int cx0 = (r - kz * nxb) * LPC;
   const int nlc = min(LPC, P0 - cx0);
   const int nt = a.nterms[yf];
-  load_tw_async<T>(tw, twg, S::L);  // constant table: overlaps the predecessor's tail
+  constexpr bool kBulkTw = inv_bulk_tw<T, S::L>();
+  __shared__ uint64_t bar;
+  if constexpr (kBulkTw) inv_bulk_start<T, S::L>(&bar, tw, twg);
+  else load_tw_async<T>(tw, twg, S::L);  // constant table: overlaps the predecessor's tail
   pdl_wait();
-  for (int t = 0; t < nt; ++t) {
-    const Cx<T>* src = a.in + a.xf[yf][t] * g.n1 + (int64_t)kz * B1 * P0 + cx0;
-    Cx<T>* dst = slab + t * B1 * LPCS;
-    for (int i = threadIdx.x; i < B1 * LPC; i += blockDim.x) {
-      const int iy = i / LPC, l = i - iy * LPC;
-      if (l < nlc) cp_async<T>(dst + iy * LPCS + l, src + iy * P0 + l);
-      BLR_CHECK(l >= nlc || (int64_t)kz * B1 * P0 + cx0 + iy * P0 + l < g.n1, "yinv src");
+  {
+    for (int t = 0; t < nt; ++t) {
+      const Cx<T>* src = a.in + a.xf[yf][t] * g.n1 + (int64_t)kz * B1 * P0 + cx0;
+      Cx<T>* dst = slab + t * B1 * LPCS;
+      for (int i = threadIdx.x; i < B1 * LPC; i += blockDim.x) {
+        const int iy = i / LPC, l = i - iy * LPC;
+        if (l < nlc) cp_async<T>(dst + iy * LPCS + l, src + iy * P0 + l);
+        BLR_CHECK(l >= nlc || (int64_t)kz * B1 * P0 + cx0 + iy * P0 + l < g.n1, "yinv src");
+      }
     }
+    __pipeline_commit();
+    if constexpr (kBulkTw) {
+      if (threadIdx.x == 0) mbar_arrive(&bar);  // the table's bytes complete the phase
+      mbar_wait(&bar, 0);
+    }
+    __pipeline_wait_prior(0);
+    __syncthreads();
   }
-  __pipeline_commit();
-  __pipeline_wait_prior(0);
-  __syncthreads();
   const int wl0 = (threadIdx.x >> 5) * S::LPW;
   const int nl = min(S::LPW, nlc - wl0);
   if (nl <= 0) return;
