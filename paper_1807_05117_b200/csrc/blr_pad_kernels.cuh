@@ -1113,6 +1113,12 @@ constexpr int kMaxYF = 24;
 #endif
 template <typename T>
 constexpr bool fwd_tw_async() { return BLR_FWD_TW_ASYNC != 0 && sizeof(T) == 4; }
+// fp64: the table by one cp.async.bulk on the first slab's mbarrier (no CTA
+// barrier at start); A/B r02: x / y forward 1.84 / 1.69 -> 1.78 / 1.61 ms per
+// deformation GN HVP (fp32 keeps the cp.async copies: bulk was 1.60 -> 1.69)
+#ifndef BLR_FWD_TW_BULK
+#define BLR_FWD_TW_BULK 1
+#endif
 template <typename T>
 struct YFwdArgs {
   const Cx<T>* sin[kMaxYF][3];
@@ -1157,7 +1163,15 @@ __global__ void __launch_bounds__(kPWF * 32, BLR_YFWD_MINB) k_yfwd(YFwdArgs<T> a
     stg.rows(slab + b * SLAB, LS, src, S::L, nlc, S::L, b);
   };
   // twiddles by cp.async in their own group, in flight with the first slab
-  if constexpr (fwd_tw_async<T>()) {
+  constexpr bool kTwBulk = BLR_FWD_TW_BULK && sizeof(T) == 8 && decltype(stg)::kBulk &&
+                           (2 * S::L * sizeof(T)) % 16 == 0;
+  if constexpr (kTwBulk) {  // on the first slab's mbarrier: its first wait covers the table
+    if (threadIdx.x == 0) {
+      const uint32_t nb = 2 * S::L * sizeof(T);
+      mbar_expect_tx_only(bars, nb);
+      bulk_g2s(tw, sizeof(T) == 8 ? (const void*)twg : (const void*)(twg + 2 * S::L), nb, bars);
+    }
+  } else if constexpr (fwd_tw_async<T>()) {
     copy_tw_async<T>(tw, twg, S::L, threadIdx.x, blockDim.x);
     __pipeline_commit();
   } else {
@@ -1169,8 +1183,8 @@ __global__ void __launch_bounds__(kPWF * 32, BLR_YFWD_MINB) k_yfwd(YFwdArgs<T> a
   if (it < nitems) issue(it, 0, 0);
   stg.commit();
   const int wl0 = (threadIdx.x >> 5) * S::LPW;
-  if constexpr (fwd_tw_async<T>()) __pipeline_wait_prior(decltype(stg)::kBulk ? 0 : 1);
-  __syncthreads();  // twiddles
+  if constexpr (!kTwBulk && fwd_tw_async<T>()) __pipeline_wait_prior(decltype(stg)::kBulk ? 0 : 1);
+  if constexpr (!kTwBulk) __syncthreads();  // twiddles
   while (it < nitems) {
     const int jb = it / per;
     const int nt = a.nterms[jb];
@@ -1404,7 +1418,15 @@ __global__ void __launch_bounds__(kPWF * 32, BLR_XFWD_MINB) k_xfwd(FwdArgs<T> a,
       }
     }
   };
-  if constexpr (fwd_tw_async<T>()) {  // as k_yfwd
+  constexpr bool kTwBulk = BLR_FWD_TW_BULK && sizeof(T) == 8 && decltype(stg)::kBulk &&
+                           (2 * S::L * sizeof(T)) % 16 == 0;
+  if constexpr (kTwBulk) {  // on the first slab's mbarrier: its first wait covers the table
+    if (threadIdx.x == 0) {
+      const uint32_t nb = 2 * S::L * sizeof(T);
+      mbar_expect_tx_only(bars, nb);
+      bulk_g2s(tw, sizeof(T) == 8 ? (const void*)twg : (const void*)(twg + 2 * S::L), nb, bars);
+    }
+  } else if constexpr (fwd_tw_async<T>()) {  // as k_yfwd
     copy_tw_async<T>(tw, twg, S::L, threadIdx.x, blockDim.x);
     __pipeline_commit();
   } else {
@@ -1417,8 +1439,8 @@ __global__ void __launch_bounds__(kPWF * 32, BLR_XFWD_MINB) k_xfwd(FwdArgs<T> a,
   stg.commit();
   const int warp = threadIdx.x >> 5;
   const int wl0 = warp * LPW;
-  if constexpr (fwd_tw_async<T>()) __pipeline_wait_prior(decltype(stg)::kBulk ? 0 : 1);
-  __syncthreads();  // twiddles
+  if constexpr (!kTwBulk && fwd_tw_async<T>()) __pipeline_wait_prior(decltype(stg)::kBulk ? 0 : 1);
+  if constexpr (!kTwBulk) __syncthreads();  // twiddles
   while (it < nitems) {
     const int o = it / per;
     const FwdOut<T>& O = a.o[o];
