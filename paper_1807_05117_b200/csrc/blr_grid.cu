@@ -347,8 +347,15 @@ struct NodeW {
   double w[kMaxNodeW];
 };
 
+#ifndef BLR_SGN_MINB
+#define BLR_SGN_MINB 4
+#endif
+#ifndef BLR_SGN_UNROLL
+#define BLR_SGN_UNROLL 4
+#endif
+constexpr int kSgnUnroll = BLR_SGN_UNROLL;
 template <typename T>
-__global__ void __launch_bounds__(256) k_state_gn(const T* __restrict__ dlam, const T* __restrict__ vol,
+__global__ void __launch_bounds__(256, BLR_SGN_MINB) k_state_gn(const T* __restrict__ dlam, const T* __restrict__ vol,
                                                   const T* __restrict__ psi, const T* __restrict__ gm,
                                                   int n_nodes, NodeW w, int interp,
                                                   FullDesc fd, int add, T* __restrict__ acc) {
@@ -357,7 +364,7 @@ __global__ void __launch_bounds__(256) k_state_gn(const T* __restrict__ dlam, co
     int x[3];
     unravel(fd, i, x);
     T s[3] = {0, 0, 0};
-#pragma unroll 4
+#pragma unroll kSgnUnroll
     for (int k = 0; k < n_nodes; ++k) {
       double c[3];
       sample_coords<T>(fd, psi + (int64_t)k * fd.d * fd.nn, i, x, c);
