@@ -21,6 +21,7 @@
 #include "blr_fft.cuh"
 #include "blr_internal.cuh"
 
+#include <cuda.h>  // CUtensorMap (the encoder is reached through the runtime's driver entry point)
 #include <cuda_pipeline_primitives.h>
 
 #include <cmath>
@@ -102,6 +103,7 @@ struct XPassArgs {
   int mulx[kMaxX];
   int nx;
   Cx<T>* out;
+  int fidx[kMaxX];  // TMA: field index of src[xf] in the tensor map (set by launch_xinv)
 };
 
 template <typename T>
@@ -168,6 +170,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 
 __device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t bytes) {  // no arrive
   asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// one TMA tile load of a rank-4 tensor map into shared memory, completing on bar
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -320,14 +331,19 @@ constexpr bool fwd_bulk_rows() {
 template <typename T, class S>
 constexpr int fwd_row_stride() { return row_stride<T, S, true, sizeof(T) == 4 && fwd_bulk_rows<T, S>()>(); }
 
-template <typename T, class S>
-__global__ void __launch_bounds__(kPW * 32) k_xinv(XPassArgs<T> a, PadGeom g, const double* __restrict__ twg) {
+// TMA (as k_yinv): the slab is one tensor-tile load, box 2 LPC x B0 of the H
+// fields viewed as [field][kz][kx][2 ky]
+template <typename T, class S, bool TMA = false>
+__global__ void __launch_bounds__(kPW * 32) k_xinv(XPassArgs<T> a, PadGeom g, const double* __restrict__ twg,
+                                                  const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int LPC = kPW * S::LPW;
   const int K0 = g.K[0], B0 = g.B[0], B1 = g.B[1];
   T* tw = (T*)smem_raw;
-  constexpr int LPCS = t_stride<LPC>();
-  Cx<T>* slab = (Cx<T>*)(tw + 2 * S::L);         // [B0][LPCS]
+  constexpr int LPCS = TMA ? LPC : t_stride<LPC>();
+  const uint32_t s0 = smem_u32(smem_raw);
+  const size_t slab_off = TMA ? (((s0 + 2 * S::L * sizeof(T) + 127) & ~127u) - s0) : 2 * S::L * sizeof(T);
+  Cx<T>* slab = (Cx<T>*)(smem_raw + slab_off);   // [B0][LPCS]
   Cx<T>* tile = slab + B0 * LPCS + (threadIdx.x >> 5) * TileG<T, S>::TILE;
   const int nyb = (B1 + LPC - 1) / LPC;
   const int per = g.Kz1 * nyb;
@@ -337,12 +353,18 @@ __global__ void __launch_bounds__(kPW * 32) k_xinv(XPassArgs<T> a, PadGeom g, co
   const int cky0 = (r - kz * nyb) * LPC;
   const int nlc = min(LPC, B1 - cky0);
   const Cx<T>* src = a.src[xf] + ((int64_t)kz * B0) * B1 + cky0;
-  constexpr bool kBulkTw = inv_bulk_tw<T, S::L>();
+  constexpr bool kBulkTw = TMA || inv_bulk_tw<T, S::L>();
   __shared__ uint64_t bar;
   if constexpr (kBulkTw) inv_bulk_start<T, S::L>(&bar, tw, twg);
   else load_tw_async<T>(tw, twg, S::L);  // constant table: overlaps the predecessor's tail
   pdl_wait();
-  {
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(&bar, (uint32_t)(B0 * 2 * LPC * sizeof(T)));
+      tma_load_4d(slab, &tmap, 2 * cky0, 0, kz, a.fidx[xf], &bar);
+    }
+    mbar_wait(&bar, 0);
+  } else {
     for (int i = threadIdx.x; i < B0 * LPC; i += blockDim.x) {
       const int ix = i / LPC, l = i - ix * LPC;
       if (l < nlc) cp_async<T>(slab + ix * LPCS + l, src + ix * B1 + l);
@@ -399,15 +421,27 @@ struct YPassArgs {
   Cx<T>* out;
 };
 
-template <typename T, class S>
-__global__ void __launch_bounds__(kPW * 32) k_yinv(YPassArgs<T> a, PadGeom g, const double* __restrict__ twg, int ntmax) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+// TMA: the slab of every term is one tensor-tile load (box 2 LPC x B1 of the
+// I fields viewed as a rank-4 tensor [field][kz][ky][2 x]) on the mbarrier,
+// dense rows (stride LPC) at a 128-byte aligned slab; out-of-range lines of
+// the last chunk are zero-filled by the copy engine.
+template <typename T, class S, bool TMA = false>
+__global__ void __launch_bounds__(kPW * 32) k_yinv(YPassArgs<T> a, PadGeom g, const double* __restrict__ twg, int ntmax,
+                                                  const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int LPC = kPW * S::LPW;
   const int P0 = g.P[0], K1 = g.K[1], B1 = g.B[1];
   T* tw = (T*)smem_raw;
-  constexpr int LPCS = t_stride<LPC>();
-  Cx<T>* slab = (Cx<T>*)(tw + 2 * S::L);         // [ntmax][B1][LPCS]
-  Cx<T>* tile = slab + ntmax * B1 * LPCS + (threadIdx.x >> 5) * TileG<T, S>::TILE;
+  constexpr int LPCS = TMA ? LPC : t_stride<LPC>();
+  // TMA destinations 128-byte aligned in the shared window (the dynamic
+  // segment itself is only guaranteed 16-byte alignment)
+  const uint32_t s0 = smem_u32(smem_raw);
+  const size_t slab_off = TMA ? (((s0 + 2 * S::L * sizeof(T) + 127) & ~127u) - s0) : 2 * S::L * sizeof(T);
+  Cx<T>* slab = (Cx<T>*)(smem_raw + slab_off);   // [ntmax][B1t][LPCS]
+  // TMA: each term's slab starts 128-byte aligned (rows padded to B1t)
+  constexpr int kRowAlign = TMA ? 128 / cgcd(128, LPC * (int)sizeof(Cx<T>)) : 1;
+  const int B1t = ((B1 + kRowAlign - 1) / kRowAlign) * kRowAlign;
+  Cx<T>* tile = slab + ntmax * B1t * LPCS + (threadIdx.x >> 5) * TileG<T, S>::TILE;
   const int nxb = (P0 + LPC - 1) / LPC;
   const int per = g.Kz1 * nxb;
   const int yf = blockIdx.x / per;
@@ -416,15 +450,21 @@ __global__ void __launch_bounds__(kPW * 32) k_yinv(YPassArgs<T> a, PadGeom g, co
   const int cx0 = (r - kz * nxb) * LPC;
   const int nlc = min(LPC, P0 - cx0);
   const int nt = a.nterms[yf];
-  constexpr bool kBulkTw = inv_bulk_tw<T, S::L>();
+  constexpr bool kBulkTw = TMA || inv_bulk_tw<T, S::L>();
   __shared__ uint64_t bar;
   if constexpr (kBulkTw) inv_bulk_start<T, S::L>(&bar, tw, twg);
   else load_tw_async<T>(tw, twg, S::L);  // constant table: overlaps the predecessor's tail
   pdl_wait();
-  {
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(&bar, (uint32_t)(nt * B1 * 2 * LPC * sizeof(T)));
+      for (int t = 0; t < nt; ++t) tma_load_4d(slab + t * B1t * LPC, &tmap, 2 * cx0, 0, kz, a.xf[yf][t], &bar);
+    }
+    mbar_wait(&bar, 0);
+  } else {
     for (int t = 0; t < nt; ++t) {
       const Cx<T>* src = a.in + a.xf[yf][t] * g.n1 + (int64_t)kz * B1 * P0 + cx0;
-      Cx<T>* dst = slab + t * B1 * LPCS;
+      Cx<T>* dst = slab + t * B1t * LPCS;
       for (int i = threadIdx.x; i < B1 * LPC; i += blockDim.x) {
         const int iy = i / LPC, l = i - iy * LPC;
         if (l < nlc) cp_async<T>(dst + iy * LPCS + l, src + iy * P0 + l);
@@ -455,7 +495,7 @@ __global__ void __launch_bounds__(kPW * 32) k_yinv(YPassArgs<T> a, PadGeom g, co
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
       if (ax[t] < -1) break;
-      Cx<T> z = slab[(t * B1 + iyc) * LPCS + wl0 + line];
+      Cx<T> z = slab[(t * B1t + iyc) * LPCS + wl0 + line];
       if (ax[t] >= 1) z = mul_ik<T>(z, ax[t] == 1 ? ky : kzk);
       acc = cadd(acc, z);
     }
@@ -1683,26 +1723,104 @@ static void ensure_smem(K kernel, size_t bytes) {
   f.smem_raised[(const void*)kernel] = true;
 }
 
+// TMA tensor maps (y-inverse slabs): the encoder comes from the driver through
+// the runtime's entry-point query, so the library needs no -lcuda
+#ifndef BLR_YINV_TMA
+#define BLR_YINV_TMA 1
+#endif
+#ifndef BLR_XINV_TMA
+#define BLR_XINV_TMA 1
+#endif
+using TmapEncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+inline TmapEncodeFn tmap_encoder() {
+  static const TmapEncodeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return (TmapEncodeFn)p;
+  }();
+  return fn;
+}
+// rank-4 map of nf fields [field][kz][ky][x0] (x0 in T units, innermost),
+// box {bx, B1, 1, 1}; false when the layout does not meet the TMA rules
+template <typename T>
+bool inv_tma_map(CUtensorMap& map, const void* base, int64_t x0, int B1, int Kz1, int nf, int64_t field, int bx) {
+  const TmapEncodeFn enc = tmap_encoder();
+  const size_t es = sizeof(T);
+  if (!enc || (x0 * es) % 16 || (bx * es) % 16 || bx > 256 || B1 > 256 || (reinterpret_cast<uintptr_t>(base) & 15))
+    return false;
+  const cuuint64_t dims[4] = {(cuuint64_t)x0, (cuuint64_t)B1, (cuuint64_t)Kz1, (cuuint64_t)nf};
+  const cuuint64_t strides[3] = {(cuuint64_t)(x0 * es), (cuuint64_t)(x0 * B1 * es), (cuuint64_t)(2 * field * es)};
+  const cuuint32_t box[4] = {(cuuint32_t)bx, (cuuint32_t)B1, 1, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(&map, es == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+             const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <typename T, class S>
-void launch_xinv(blr_ctx* c, PadEngine* e, const XPassArgs<T>& a) {
+void launch_xinv(blr_ctx* c, PadEngine* e, const XPassArgs<T>& a0) {
   const PadGeom& g = e->g;
   constexpr int LPC = kPW * S::LPW;
+  const int nyb = (g.B[1] + LPC - 1) / LPC;
+  XPassArgs<T> a = a0;
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof(map));
+  // TMA when every source is base + k * nh (one rank-4 map over the fields)
+  bool tma = BLR_XINV_TMA && (2 * S::L * sizeof(T)) % 16 == 0 && a.nx > 0;
+  const Cx<T>* base = a.src[0];
+  for (int i = 0; i < a.nx && tma; ++i) base = std::min(base, a.src[i]);
+  int nf = 1;
+  for (int i = 0; i < a.nx && tma; ++i) {
+    const int64_t d = a.src[i] - base;
+    tma = d % g.nh == 0 && d / g.nh < (1 << 20);
+    a.fidx[i] = tma ? (int)(d / g.nh) : 0;
+    nf = std::max(nf, a.fidx[i] + 1);
+  }
+  if (tma && inv_tma_map<T>(map, base, 2 * (int64_t)g.B[1], g.B[0], g.Kz1, nf, g.nh, 2 * LPC)) {
+    const size_t sm = 2 * S::L * sizeof(T) + 128 + sizeof(Cx<T>) * ((size_t)g.B[0] * LPC + kPW * TileG<T, S>::TILE);
+    ensure_smem(k_xinv<T, S, true>, sm);
+    launch_pdl(k_xinv<T, S, true>, a.nx * g.Kz1 * nyb, kPW * 32, sm, c->stream, a, g, (const double*)e->tw[0], map);
+    BLR_LAUNCHED();
+    return;
+  }
   const size_t sm = sizeof(Cx<T>) * (S::L + (size_t)g.B[0] * t_stride<LPC>() + kPW * TileG<T, S>::TILE);
   ensure_smem(k_xinv<T, S>, sm);
-  const int nyb = (g.B[1] + LPC - 1) / LPC;
-  launch_pdl(k_xinv<T, S>, a.nx * g.Kz1 * nyb, kPW * 32, sm, c->stream, a, g, (const double*)e->tw[0]);
+  launch_pdl(k_xinv<T, S>, a.nx * g.Kz1 * nyb, kPW * 32, sm, c->stream, a, g, (const double*)e->tw[0], map);
   BLR_LAUNCHED();
 }
 template <typename T, class S>
 void launch_yinv(blr_ctx* c, PadEngine* e, const YPassArgs<T>& a) {
   const PadGeom& g = e->g;
   constexpr int LPC = kPW * S::LPW;
-  int ntmax = 1;
-  for (int i = 0; i < a.ny; ++i) ntmax = std::max(ntmax, a.nterms[i]);
+  int ntmax = 1, nf = 1;
+  for (int i = 0; i < a.ny; ++i) {
+    ntmax = std::max(ntmax, a.nterms[i]);
+    for (int t = 0; t < a.nterms[i]; ++t) nf = std::max(nf, a.xf[i][t] + 1);
+  }
+  const int nxb = (g.P[0] + LPC - 1) / LPC;
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof(map));
+  if (BLR_YINV_TMA && (2 * S::L * sizeof(T)) % 16 == 0 &&
+      inv_tma_map<T>(map, a.in, 2 * (int64_t)g.P[0], g.B[1], g.Kz1, nf, g.n1, 2 * LPC)) {
+    constexpr int ra = 128 / cgcd(128, LPC * (int)sizeof(Cx<T>));
+    const size_t b1t = ((g.B[1] + ra - 1) / ra) * ra;
+    const size_t sm = 2 * S::L * sizeof(T) + 128 +  // + alignment slack of the slab
+                      sizeof(Cx<T>) * ((size_t)ntmax * b1t * LPC + kPW * TileG<T, S>::TILE);
+    ensure_smem(k_yinv<T, S, true>, sm);
+    launch_pdl(k_yinv<T, S, true>, a.ny * g.Kz1 * nxb, kPW * 32, sm, c->stream, a, g, (const double*)e->tw[1], ntmax,
+               map);
+    BLR_LAUNCHED();
+    return;
+  }
   const size_t sm = sizeof(Cx<T>) * (S::L + (size_t)ntmax * g.B[1] * t_stride<LPC>() + kPW * TileG<T, S>::TILE);
   ensure_smem(k_yinv<T, S>, sm);
-  const int nxb = (g.P[0] + LPC - 1) / LPC;
-  launch_pdl(k_yinv<T, S>, a.ny * g.Kz1 * nxb, kPW * 32, sm, c->stream, a, g, (const double*)e->tw[1], ntmax);
+  launch_pdl(k_yinv<T, S>, a.ny * g.Kz1 * nxb, kPW * 32, sm, c->stream, a, g, (const double*)e->tw[1], ntmax, map);
   BLR_LAUNCHED();
 }
 template <typename T, class S, int OP>
