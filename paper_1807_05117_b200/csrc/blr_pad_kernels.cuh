@@ -1728,8 +1728,11 @@ static void ensure_smem(K kernel, size_t bytes) {
 #ifndef BLR_YINV_TMA
 #define BLR_YINV_TMA 1
 #endif
+// x-inverse TMA: opt-in (build flag); A/B r02: 128^3 x-inverse 0.99 -> 0.98 ms
+// (deformation 8.50 -> 8.48 ms) but 256^3 (L = 196, 128-byte box rows) 7.45 ->
+// 8.21 ms per HVP
 #ifndef BLR_XINV_TMA
-#define BLR_XINV_TMA 1
+#define BLR_XINV_TMA 0
 #endif
 using TmapEncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
