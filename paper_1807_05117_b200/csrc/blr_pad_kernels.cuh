@@ -91,6 +91,26 @@ __device__ __forceinline__ bool load_tw_async(T* dst, const double* src, int L) 
 template <typename T>
 __device__ __forceinline__ Cx<T> mul_ik(Cx<T> z, T k) { return cx<T>(-(k * z.y), k * z.x); }
 
+// n / d for 0 <= n < 2^23 and a divisor fixed per kernel: a float reciprocal
+// estimate (off by at most one) and one correction, instead of the ~20-
+// instruction integer division sequence (the persistent passes divide item
+// indices several times per item).  BLR_FDIV=0: plain division.
+#ifndef BLR_FDIV
+#define BLR_FDIV 1
+#endif
+struct FDiv {
+  int d;
+  float r;
+  __device__ __forceinline__ explicit FDiv(int dd) : d(dd), r(1.0f / (float)dd) {}
+  __device__ __forceinline__ int operator()(int n) const {
+    if constexpr (!BLR_FDIV) return n / d;
+    int q = __float2int_rz((float)n * r);
+    const int rem = n - q * d;
+    q += (rem >= d) - (rem < 0);
+    return q;
+  }
+};
+
 // ---------------------------------------------------------------------------
 // inverse x pass: band H [kz][kx][ky] -> I [xf][kz][ky][x]
 // ---------------------------------------------------------------------------
@@ -1187,15 +1207,16 @@ __global__ void __launch_bounds__(kPWF * 32, BLR_YFWD_MINB) k_yfwd(YFwdArgs<T> a
   Cx<T>* res = slab + 2 * SLAB;                  // [B1][LPCS] job accumulator
   const int nxb = (P0 + LPC - 1) / LPC;
   const int per = g.Kz1 * nxb;
+  const FDiv div_per(per), div_nxb(nxb);
   const int nitems = a.nj * per;
   __shared__ uint64_t bars[2];
   Stager<T, fwd_bulk_rows<T, S>()> stg;
   stg.init(bars);
   __syncthreads();
   auto issue = [&](int it, int t, int b) {
-    const int jb = it / per;
+    const int jb = div_per(it);
     const int r = it - jb * per;
-    const int kz = r / nxb;
+    const int kz = div_nxb(r);
     const int cx0 = (r - kz * nxb) * LPC;
     const int nlc = min(LPC, P0 - cx0);
     const Cx<T>* src = a.sin[jb][t] + ((int64_t)kz * P0 + cx0) * S::L;  // nlc contiguous rows
@@ -1226,7 +1247,7 @@ __global__ void __launch_bounds__(kPWF * 32, BLR_YFWD_MINB) k_yfwd(YFwdArgs<T> a
   if constexpr (!kTwBulk && fwd_tw_async<T>()) __pipeline_wait_prior(decltype(stg)::kBulk ? 0 : 1);
   if constexpr (!kTwBulk) __syncthreads();  // twiddles
   while (it < nitems) {
-    const int jb = it / per;
+    const int jb = div_per(it);
     const int nt = a.nterms[jb];
     int nit = it, ntt = t + 1;
     if (ntt >= nt) { nit = it + gridDim.x; ntt = 0; }
@@ -1234,7 +1255,7 @@ __global__ void __launch_bounds__(kPWF * 32, BLR_YFWD_MINB) k_yfwd(YFwdArgs<T> a
     stg.commit();
     stg.wait(b);
     const int r = it - jb * per;
-    const int kz = r / nxb;
+    const int kz = div_nxb(r);
     const int cx0 = (r - kz * nxb) * LPC;
     const int nl = min(S::LPW, min(LPC, P0 - cx0) - wl0);
     if (nl > 0) {
@@ -1385,6 +1406,7 @@ __global__ void __launch_bounds__(kPWF * 32, BLR_XFWD_MINB) k_xfwd(FwdArgs<T> a,
   const int nyb = (B1 + LPC - 1) / LPC;
   const int n0 = (K1 + 1 + LPW - 1) / LPW;      // kz = 0 items (LPW mirror units each)
   const int per = n0 + (g.Kz1 - 1) * nyb;
+  const FDiv div_per(per), div_nyb(nyb);
   const int nitems = a.no * per;
   // item r of an output -> kz, first ky (kz > 0) or first unit p0 and the two half sizes (kz = 0)
   struct Item { int kz, cky0, p0, c1, c2; };
@@ -1398,8 +1420,9 @@ __global__ void __launch_bounds__(kPWF * 32, BLR_XFWD_MINB) k_xfwd(FwdArgs<T> a,
       m.c2 = m.p0 == 0 ? m.c1 - 1 : m.c1;  // unit 0 (ky = 0) is its own mirror
     } else {
       const int q = r - n0;
-      m.kz = 1 + q / nyb;
-      m.cky0 = (q - (q / nyb) * nyb) * LPC;
+      const int qk = div_nyb(q);
+      m.kz = 1 + qk;
+      m.cky0 = (q - qk * nyb) * LPC;
       m.p0 = -1;
       m.c1 = min(LPC, B1 - m.cky0);
       m.c2 = 0;
@@ -1421,7 +1444,7 @@ __global__ void __launch_bounds__(kPWF * 32, BLR_XFWD_MINB) k_xfwd(FwdArgs<T> a,
   stg.init(bars);
   __syncthreads();
   auto issue = [&](int it, int t, int b) {
-    const int o = it / per;
+    const int o = div_per(it);
     const Item m = decode(it - o * per);
     const Cx<T>* base = a.in + a.o[o].f[t] * g.n1 + (int64_t)m.kz * B1 * S::L;
     Cx<T>* dst = slab + b * SLAB;
@@ -1442,7 +1465,7 @@ __global__ void __launch_bounds__(kPWF * 32, BLR_XFWD_MINB) k_xfwd(FwdArgs<T> a,
   // stalling the epilogue.  Rows are read only by this item (no staleness).
   auto prefetch_epi = [&](int it_) {
     if constexpr (kXfwdPrefetch) {
-      const int o = it_ / per;
+      const int o = div_per(it_);
       const Item m = decode(it_ - o * per);
       if (m.kz == 0) return;  // mirror items: scattered rows
       const FwdOut<T>& O = a.o[o];
@@ -1482,7 +1505,7 @@ __global__ void __launch_bounds__(kPWF * 32, BLR_XFWD_MINB) k_xfwd(FwdArgs<T> a,
   if constexpr (!kTwBulk && fwd_tw_async<T>()) __pipeline_wait_prior(decltype(stg)::kBulk ? 0 : 1);
   if constexpr (!kTwBulk) __syncthreads();  // twiddles
   while (it < nitems) {
-    const int o = it / per;
+    const int o = div_per(it);
     const FwdOut<T>& O = a.o[o];
     const int nt = O.nterms;
     int nit = it, ntt = t + 1;
