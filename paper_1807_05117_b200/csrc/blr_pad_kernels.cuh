@@ -288,13 +288,17 @@ struct Stager {
   }
 };
 
-// Staged pass kernels: kPW warps per CTA; the CTA's whole input slab is
+// Staged pass kernels: inv_pw<T>() warps per CTA; the CTA's whole input slab is
 // copied to shared memory with coalesced cp.async first, then every warp runs
 // its four-step FFTs from shared memory.
+// warps per CTA of the inverse passes: fp64 2, fp32 4 (A/B r02 with TMA-staged
+// slabs: fp64 deformation / state 8.45 / 4.73 -> 8.38 / 4.67 ms at 2 warps,
+// 8.82 / 4.92 at 8; fp32 5.85 -> 5.88 at 2); BLR_KPW=n forces n
 #ifndef BLR_KPW
-#define BLR_KPW 4
+#define BLR_KPW 0
 #endif
-constexpr int kPW = BLR_KPW;  // inverse passes (x, y)
+template <typename T>
+constexpr int inv_pw() { return BLR_KPW ? BLR_KPW : (sizeof(T) == 8 ? 2 : 4); }
 constexpr int kPWF = 2;  // forward passes (y, x): measured best at 2 warps per CTA
 
 // Shared-memory strides chosen so the FFT access patterns are free of bank
@@ -354,10 +358,10 @@ constexpr int fwd_row_stride() { return row_stride<T, S, true, sizeof(T) == 4 &&
 // TMA (as k_yinv): the slab is one tensor-tile load, box 2 LPC x B0 of the H
 // fields viewed as [field][kz][kx][2 ky]
 template <typename T, class S, bool TMA = false>
-__global__ void __launch_bounds__(kPW * 32) k_xinv(XPassArgs<T> a, PadGeom g, const double* __restrict__ twg,
+__global__ void __launch_bounds__(inv_pw<T>() * 32) k_xinv(XPassArgs<T> a, PadGeom g, const double* __restrict__ twg,
                                                   const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int LPC = kPW * S::LPW;
+  constexpr int LPC = inv_pw<T>() * S::LPW;
   const int K0 = g.K[0], B0 = g.B[0], B1 = g.B[1];
   T* tw = (T*)smem_raw;
   constexpr int LPCS = TMA ? LPC : t_stride<LPC>();
@@ -446,10 +450,10 @@ struct YPassArgs {
 // dense rows (stride LPC) at a 128-byte aligned slab; out-of-range lines of
 // the last chunk are zero-filled by the copy engine.
 template <typename T, class S, bool TMA = false>
-__global__ void __launch_bounds__(kPW * 32) k_yinv(YPassArgs<T> a, PadGeom g, const double* __restrict__ twg, int ntmax,
+__global__ void __launch_bounds__(inv_pw<T>() * 32) k_yinv(YPassArgs<T> a, PadGeom g, const double* __restrict__ twg, int ntmax,
                                                   const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  constexpr int LPC = kPW * S::LPW;
+  constexpr int LPC = inv_pw<T>() * S::LPW;
   const int P0 = g.P[0], K1 = g.K[1], B1 = g.B[1];
   T* tw = (T*)smem_raw;
   constexpr int LPCS = TMA ? LPC : t_stride<LPC>();
@@ -1797,7 +1801,7 @@ bool inv_tma_map(CUtensorMap& map, const void* base, int64_t x0, int B1, int Kz1
 template <typename T, class S>
 void launch_xinv(blr_ctx* c, PadEngine* e, const XPassArgs<T>& a0) {
   const PadGeom& g = e->g;
-  constexpr int LPC = kPW * S::LPW;
+  constexpr int LPC = inv_pw<T>() * S::LPW;
   const int nyb = (g.B[1] + LPC - 1) / LPC;
   XPassArgs<T> a = a0;
   CUtensorMap map;
@@ -1814,21 +1818,21 @@ void launch_xinv(blr_ctx* c, PadEngine* e, const XPassArgs<T>& a0) {
     nf = std::max(nf, a.fidx[i] + 1);
   }
   if (tma && inv_tma_map<T>(map, base, 2 * (int64_t)g.B[1], g.B[0], g.Kz1, nf, g.nh, 2 * LPC)) {
-    const size_t sm = 2 * S::L * sizeof(T) + 128 + sizeof(Cx<T>) * ((size_t)g.B[0] * LPC + kPW * TileG<T, S>::TILE);
+    const size_t sm = 2 * S::L * sizeof(T) + 128 + sizeof(Cx<T>) * ((size_t)g.B[0] * LPC + inv_pw<T>() * TileG<T, S>::TILE);
     ensure_smem(k_xinv<T, S, true>, sm);
-    launch_pdl(k_xinv<T, S, true>, a.nx * g.Kz1 * nyb, kPW * 32, sm, c->stream, a, g, (const double*)e->tw[0], map);
+    launch_pdl(k_xinv<T, S, true>, a.nx * g.Kz1 * nyb, inv_pw<T>() * 32, sm, c->stream, a, g, (const double*)e->tw[0], map);
     BLR_LAUNCHED();
     return;
   }
-  const size_t sm = sizeof(Cx<T>) * (S::L + (size_t)g.B[0] * t_stride<LPC>() + kPW * TileG<T, S>::TILE);
+  const size_t sm = sizeof(Cx<T>) * (S::L + (size_t)g.B[0] * t_stride<LPC>() + inv_pw<T>() * TileG<T, S>::TILE);
   ensure_smem(k_xinv<T, S>, sm);
-  launch_pdl(k_xinv<T, S>, a.nx * g.Kz1 * nyb, kPW * 32, sm, c->stream, a, g, (const double*)e->tw[0], map);
+  launch_pdl(k_xinv<T, S>, a.nx * g.Kz1 * nyb, inv_pw<T>() * 32, sm, c->stream, a, g, (const double*)e->tw[0], map);
   BLR_LAUNCHED();
 }
 template <typename T, class S>
 void launch_yinv(blr_ctx* c, PadEngine* e, const YPassArgs<T>& a) {
   const PadGeom& g = e->g;
-  constexpr int LPC = kPW * S::LPW;
+  constexpr int LPC = inv_pw<T>() * S::LPW;
   int ntmax = 1, nf = 1;
   for (int i = 0; i < a.ny; ++i) {
     ntmax = std::max(ntmax, a.nterms[i]);
@@ -1842,16 +1846,16 @@ void launch_yinv(blr_ctx* c, PadEngine* e, const YPassArgs<T>& a) {
     constexpr int ra = 128 / cgcd(128, LPC * (int)sizeof(Cx<T>));
     const size_t b1t = ((g.B[1] + ra - 1) / ra) * ra;
     const size_t sm = 2 * S::L * sizeof(T) + 128 +  // + alignment slack of the slab
-                      sizeof(Cx<T>) * ((size_t)ntmax * b1t * LPC + kPW * TileG<T, S>::TILE);
+                      sizeof(Cx<T>) * ((size_t)ntmax * b1t * LPC + inv_pw<T>() * TileG<T, S>::TILE);
     ensure_smem(k_yinv<T, S, true>, sm);
-    launch_pdl(k_yinv<T, S, true>, a.ny * g.Kz1 * nxb, kPW * 32, sm, c->stream, a, g, (const double*)e->tw[1], ntmax,
+    launch_pdl(k_yinv<T, S, true>, a.ny * g.Kz1 * nxb, inv_pw<T>() * 32, sm, c->stream, a, g, (const double*)e->tw[1], ntmax,
                map);
     BLR_LAUNCHED();
     return;
   }
-  const size_t sm = sizeof(Cx<T>) * (S::L + (size_t)ntmax * g.B[1] * t_stride<LPC>() + kPW * TileG<T, S>::TILE);
+  const size_t sm = sizeof(Cx<T>) * (S::L + (size_t)ntmax * g.B[1] * t_stride<LPC>() + inv_pw<T>() * TileG<T, S>::TILE);
   ensure_smem(k_yinv<T, S>, sm);
-  launch_pdl(k_yinv<T, S>, a.ny * g.Kz1 * nxb, kPW * 32, sm, c->stream, a, g, (const double*)e->tw[1], ntmax, map);
+  launch_pdl(k_yinv<T, S>, a.ny * g.Kz1 * nxb, inv_pw<T>() * 32, sm, c->stream, a, g, (const double*)e->tw[1], ntmax, map);
   BLR_LAUNCHED();
 }
 template <typename T, class S, int OP>
